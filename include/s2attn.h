@@ -1,0 +1,238 @@
+/*
+ * s2attn.h — C ABI of the B200-native S2-Attention hot path.
+ *
+ * This is the drop-in boundary. The reference
+ * (`shardattn`, /root/reference/proj) exposes a C++ API with std::vector and
+ * exceptions and no FFI; every entry point below replaces one reference
+ * symbol (cited per function) with a plain-C equivalent: POD structs, plain
+ * pointers and sizes, int status codes, a thread-local error string, caller-
+ * owned device buffers and an explicit CUDA stream.  The C++ shim in
+ * include/shardattn_b200/ rebuilds the reference's exact `shardattn::`
+ * signatures on top of this header.
+ *
+ * Tensor layouts (device memory, row-major, contiguous):
+ *   q, out, dq, dout : [batch, num_heads,    seq_len, head_dim]
+ *   k, v, dk, dv     : [batch, num_kv_heads, seq_len, head_dim]
+ *   lse              : [batch, num_heads, seq_len] float32, natural log
+ * The reference has no batch and no GQA in its tensors
+ * (attention.hpp:17-37, idx=(h*N+t)*d+c); batch=1, num_kv_heads=num_heads
+ * reproduces that layout exactly.
+ */
+#ifndef S2ATTN_H_
+#define S2ATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define S2_ABI_VERSION 1
+#define S2_MAX_SEGMENTS 8
+
+/* ---- status codes ------------------------------------------------------ */
+/* The reference throws std::invalid_argument for every contract violation
+ * (pattern.cpp:36-79, csr.cpp:11-33, kernel_common.hpp:20-41,
+ * attention.cpp:102-110).  Those all map to S2_ERR_INVALID_ARGUMENT here;
+ * the shim turns that code back into std::invalid_argument. */
+enum {
+    S2_OK = 0,
+    S2_ERR_INVALID_ARGUMENT = 1,
+    S2_ERR_CUDA = 2,
+    S2_ERR_UNSUPPORTED = 3,
+    S2_ERR_NO_DEVICE = 4,
+    S2_ERR_OUT_OF_MEMORY = 5
+};
+
+/* Message for the last non-zero status returned on this thread. */
+const char* s2_last_error(void);
+int s2_abi_version(void);
+
+/* ---- element types ----------------------------------------------------- */
+enum {
+    S2_DTYPE_BF16 = 0, /* tcgen05 path: bf16 operands, fp32 accumulate in TMEM */
+    S2_DTYPE_F32 = 1   /* reference-precision path: fp32 storage, fp32 FFMA   */
+};
+
+typedef struct CUstream_st* s2_stream_t; /* == cudaStream_t */
+
+/* ---- layout policy ----------------------------------------------------- */
+/* POD mirror of shardattn::StrideSegment / PatternConfig
+ * (pattern.hpp:17-60).  offsets == NULL / num_offsets == 0 means the
+ * HeadModStride scheme (o_h = group_of(h) mod stride, pattern.cpp:25-33). */
+typedef struct s2_stride_segment {
+    int start_block_distance;
+    int end_block_distance;
+    int stride;
+    int num_offsets;    /* 0, num_heads or num_kv_heads */
+    const int* offsets; /* host pointer, read during the call only */
+} s2_stride_segment;
+
+typedef struct s2_pattern_config {
+    int seq_len;      /* N tokens */
+    int block_size;   /* S tokens per block; B = ceil(N/S) */
+    int num_heads;    /* H */
+    int num_kv_heads; /* 0 means num_heads */
+    int local_blocks;
+    int local_stride;
+    int num_segments;
+    s2_stride_segment segments[S2_MAX_SEGMENTS];
+} s2_pattern_config;
+
+/* Fills cfg like make_single_stride_config (pattern.cpp:190-204): one segment
+ * {local_blocks, B, remote_stride} when local_blocks < B.  Validates. */
+int s2_make_single_stride_config(int seq_len, int block_size, int num_heads, int local_blocks,
+                                 int remote_stride, int local_stride, s2_pattern_config* cfg);
+
+/* PatternConfig::validate (pattern.cpp:36-79). */
+int s2_pattern_validate(const s2_pattern_config* cfg);
+/* PatternConfig::num_blocks (pattern.cpp:12-14). */
+int s2_pattern_num_blocks(const s2_pattern_config* cfg);
+/* PatternConfig::offset_for (pattern.cpp:16-34). */
+int s2_pattern_offset_for(const s2_pattern_config* cfg, int segment, int head, int* offset);
+
+/* ---- host layout builder (analytic, O(nnz)) ----------------------------- */
+/* Bit-exact to to_csr(build_head_mask(cfg, head)) (csr.cpp:35-47,
+ * pattern.cpp:127-158) without materialising the B x B mask. */
+int s2_layout_nnz(const s2_pattern_config* cfg, int head, int64_t* nnz);
+/* row_ptr: B+1 ints; col_idx: nnz ints, ascending within each row. */
+int s2_layout_build_csr(const s2_pattern_config* cfg, int head, int* row_ptr, int* col_idx);
+/* Transpose of the same bits (no reference symbol; backward layout):
+ * col_ptr: B+1 ints; row_idx: nnz ints, ascending within each column. */
+int s2_layout_build_csc(const s2_pattern_config* cfg, int head, int* col_ptr, int* row_idx);
+/* HeadCacheSchedule::evict_after (analysis.cpp:76-82): per key block the last
+ * query block attending it.  evict_after: B ints. */
+int s2_layout_evict_after(const s2_pattern_config* cfg, int head, int* evict_after);
+/* check_kv_cache_efficiency (verify.cpp:53-72): *ok = 1 when every column's
+ * attending rows form one interval starting at the diagonal. */
+int s2_layout_kv_efficient(const s2_pattern_config* cfg, int head, int* ok);
+/* CsrMask::validate (csr.cpp:11-33). */
+int s2_csr_validate(int num_blocks, const int* row_ptr, const int* col_idx, int64_t nnz);
+
+/* ---- plans: device-resident layout + tile work lists -------------------- */
+typedef struct s2_plan s2_plan;
+
+/* From a policy (the north_star path). */
+int s2_plan_create(const s2_pattern_config* cfg, s2_plan** plan);
+/* From caller CSR lists, one per head (the shim path for
+ * streaming_sharded_attention(t, vector<CsrMask>, block_size),
+ * attention.cpp:100-118, with the same validation). row_ptr[h]: B+1 ints,
+ * col_idx[h]: row_ptr[h][B] ints.  GQA heads of a group must share bits. */
+int s2_plan_create_from_csr(int num_heads, int num_kv_heads, int seq_len, int block_size,
+                            const int* const* row_ptr, const int* const* col_idx,
+                            s2_plan** plan);
+void s2_plan_destroy(s2_plan* plan);
+
+typedef struct s2_plan_stats {
+    int num_heads, num_kv_heads, seq_len, block_size, num_blocks;
+    int64_t nnz_total;        /* sum over heads of active block pairs */
+    int64_t dense_pairs;      /* B(B+1)/2 per head, summed */
+    int max_row_len, max_col_len;
+    int64_t fwd_tiles;        /* (head, 128-row q tile) work items */
+    int64_t fwd_chunk_visits; /* 64-key chunks visited by the fwd kernel */
+    int64_t bwd_tiles;        /* (kv-group, 128-key tile) work items */
+    int64_t bwd_qtile_visits; /* q tiles visited by the dK/dV kernel */
+} s2_plan_stats;
+int s2_plan_get_stats(const s2_plan* plan, s2_plan_stats* stats);
+/* Introspection of the tile work lists (tests, tooling).  Pass NULL arrays to
+ * query the sizes.  fwd: offsets [H * num_qtiles + 1], chunk / mask per entry.
+ * bwd: tiles [5 * num_tiles] = {group, c0, c1, offset, count},
+ * entries [3 * num_entries] = {qtile, mask0, mask1}. */
+int s2_plan_fwd_tiles(s2_plan* plan, int* num_qtiles, int64_t* num_entries, int64_t* offsets,
+                      int32_t* chunks, uint32_t* masks);
+int s2_plan_bwd_tiles(s2_plan* plan, int64_t* num_tiles, int64_t* num_entries, int64_t* tiles,
+                      int64_t* entries);
+/* Active block pairs of one head (exact_flops' nnz_per_head, analysis.cpp:46-48). */
+int s2_plan_head_nnz(const s2_plan* plan, int head, int64_t* nnz);
+
+/* ---- forward ------------------------------------------------------------ */
+/* Replaces streaming_sharded_attention / dsplit_attention
+ * (attention.cpp:190-198).  num_splits is validated exactly like the
+ * reference (>= 1 and divides head_dim, attention.cpp:109-110); the GPU
+ * kernel's accumulation order does not depend on it, so dsplit(1) and
+ * streaming are bit-identical as the reference requires
+ * (test_attention.cpp:124-132).
+ *
+ * Units: the head-parallel partitioner works on (batch, kv-group) units,
+ * u = b*num_kv_heads + g.  unit_ids == NULL processes every unit and the
+ * tensors have the full layout above; otherwise the tensors hold only the
+ * listed units, packed unit-major: q/out [num_units, H/Hkv, N, D],
+ * k/v [num_units, N, D], lse [num_units, H/Hkv, N]. */
+typedef struct s2_attn_args {
+    int dtype;
+    int batch, num_heads, num_kv_heads, seq_len, head_dim;
+    double scale; /* 0 => 1/sqrt(head_dim) as AttentionTensors::zeros */
+    int num_splits;
+    int num_units;       /* ignored when unit_ids == NULL */
+    const int* unit_ids; /* host */
+    const void* q;
+    const void* k;
+    const void* v;
+    void* out;
+    float* lse;
+} s2_attn_args;
+int s2_attn_fwd(s2_plan* plan, const s2_attn_args* args, s2_stream_t stream);
+
+/* ---- backward (no reference symbol: SPEC.md:262) ------------------------ */
+/* dQ kernel walks the CSR tile list, dK/dV kernel walks the transposed (CSC)
+ * tile list; every dK/dV tile is owned by exactly one CTA (no atomics). */
+typedef struct s2_attn_bwd_args {
+    s2_attn_args fwd; /* q, k, v, out (forward output), lse as written by fwd */
+    const void* dout;
+    void* dq;
+    void* dk;
+    void* dv;
+} s2_attn_bwd_args;
+int s2_attn_bwd_workspace_size(const s2_plan* plan, const s2_attn_bwd_args* args, size_t* bytes);
+int s2_attn_bwd(s2_plan* plan, const s2_attn_bwd_args* args, void* workspace,
+                size_t workspace_bytes, s2_stream_t stream);
+
+/* ---- decode over a per-(batch, kv-head) compacted KV cache --------------- */
+/* Cache contents follow simulate_decode_cache (analysis.cpp:57-104): key
+ * block j is kept while the decode row bt <= evict_after[j]; for KV-efficient
+ * masks (verify.cpp:53-72) the kept set is exactly row bt of the mask, so the
+ * cache stores only the blocks each head can attend.  Non-efficient masks are
+ * rejected with S2_ERR_UNSUPPORTED. */
+typedef struct s2_kvcache s2_kvcache;
+int s2_kvcache_create(s2_plan* plan, int batch, int head_dim, int dtype, s2_kvcache** cache);
+void s2_kvcache_destroy(s2_kvcache* cache);
+/* Number of tokens currently held per sequence (= next position). */
+int s2_kvcache_length(const s2_kvcache* cache, int* length);
+/* Physical device bytes of the pool and the bytes a dense cache would need. */
+int s2_kvcache_bytes(const s2_kvcache* cache, int64_t* pool_bytes, int64_t* dense_bytes);
+/* Retained tokens per sequence per kv head at the current length. */
+int s2_kvcache_retained_tokens(const s2_kvcache* cache, int kv_head, int64_t* tokens);
+/* Compacts a dense prefix k/v [batch, Hkv, num_tokens, D] (device) into the
+ * cache (kv_compact kernel); resets the length to num_tokens. */
+int s2_kvcache_prefill(s2_kvcache* cache, const void* k, const void* v, int num_tokens,
+                       s2_stream_t stream);
+/* Appends one token per sequence, k/v [batch, Hkv, D] (kv_append kernel). */
+int s2_kvcache_append(s2_kvcache* cache, const void* k, const void* v, s2_stream_t stream);
+/* One query row per (batch, head) at position length-1: q/out [batch, H, D],
+ * lse [batch, H] (may be NULL).  Split-KV kernel + lse-weighted combine. */
+int s2_attn_decode_workspace_size(const s2_kvcache* cache, size_t* bytes);
+int s2_attn_decode(s2_kvcache* cache, const void* q, void* out, float* lse, double scale,
+                   void* workspace, size_t workspace_bytes, s2_stream_t stream);
+/* Bytes the decode step must read from HBM at the current length (K,V of the
+ * retained tokens + q + out): the roofline numerator. */
+int s2_attn_decode_bytes(const s2_kvcache* cache, int64_t* bytes);
+
+/* ---- head-parallel partitioner (no reference symbol) -------------------- */
+/* Weight of every (batch, kv-group) unit = active block pairs of its heads. */
+int s2_plan_unit_weights(const s2_plan* plan, int batch, int64_t* weights);
+/* LPT: units sorted by weight descending (ties by id), each to the least
+ * loaded rank (ties to the lowest rank).  owner: num_units ints; load:
+ * num_ranks int64 (may be NULL).  Deterministic. */
+int s2_partition_lpt(int num_units, const int64_t* weights, int num_ranks, int* owner,
+                     int64_t* load);
+
+/* ---- FLOP / byte accounting (analysis.cpp:29-55) ------------------------ */
+/* 4 * head_dim * block_size^2 per active pair, summed over heads and batch. */
+int s2_plan_fwd_flops(const s2_plan* plan, int batch, int head_dim, double* active_flops,
+                      double* dense_causal_flops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* S2ATTN_H_ */

@@ -1,0 +1,153 @@
+"""ctypes binding of include/s2attn.h (the C ABI of libs2attn.so).
+
+The library must exist in-tree (built by __graft_entry__.build() /
+`make -C paper_2407_17678_b200/csrc`); there is no fallback of any kind.
+"""
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libs2attn.so")
+
+S2_OK = 0
+S2_ERR_INVALID_ARGUMENT = 1
+S2_ERR_CUDA = 2
+S2_ERR_UNSUPPORTED = 3
+S2_ERR_NO_DEVICE = 4
+S2_ERR_OUT_OF_MEMORY = 5
+S2_MAX_SEGMENTS = 8
+
+S2_DTYPE_BF16 = 0
+S2_DTYPE_F32 = 1
+
+
+class s2_stride_segment(ctypes.Structure):
+    _fields_ = [("start_block_distance", ctypes.c_int), ("end_block_distance", ctypes.c_int),
+                ("stride", ctypes.c_int), ("num_offsets", ctypes.c_int),
+                ("offsets", ctypes.POINTER(ctypes.c_int))]
+
+
+class s2_pattern_config(ctypes.Structure):
+    _fields_ = [("seq_len", ctypes.c_int), ("block_size", ctypes.c_int),
+                ("num_heads", ctypes.c_int), ("num_kv_heads", ctypes.c_int),
+                ("local_blocks", ctypes.c_int), ("local_stride", ctypes.c_int),
+                ("num_segments", ctypes.c_int),
+                ("segments", s2_stride_segment * S2_MAX_SEGMENTS)]
+
+
+class s2_plan_stats(ctypes.Structure):
+    _fields_ = [("num_heads", ctypes.c_int), ("num_kv_heads", ctypes.c_int),
+                ("seq_len", ctypes.c_int), ("block_size", ctypes.c_int),
+                ("num_blocks", ctypes.c_int), ("nnz_total", ctypes.c_int64),
+                ("dense_pairs", ctypes.c_int64), ("max_row_len", ctypes.c_int),
+                ("max_col_len", ctypes.c_int), ("fwd_tiles", ctypes.c_int64),
+                ("fwd_chunk_visits", ctypes.c_int64), ("bwd_tiles", ctypes.c_int64),
+                ("bwd_qtile_visits", ctypes.c_int64)]
+
+
+class s2_attn_args(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int), ("batch", ctypes.c_int), ("num_heads", ctypes.c_int),
+                ("num_kv_heads", ctypes.c_int), ("seq_len", ctypes.c_int),
+                ("head_dim", ctypes.c_int), ("scale", ctypes.c_double),
+                ("num_splits", ctypes.c_int), ("num_units", ctypes.c_int),
+                ("unit_ids", ctypes.POINTER(ctypes.c_int)),
+                ("q", ctypes.c_void_p), ("k", ctypes.c_void_p), ("v", ctypes.c_void_p),
+                ("out", ctypes.c_void_p), ("lse", ctypes.c_void_p)]
+
+
+class s2_attn_bwd_args(ctypes.Structure):
+    _fields_ = [("fwd", s2_attn_args), ("dout", ctypes.c_void_p), ("dq", ctypes.c_void_p),
+                ("dk", ctypes.c_void_p), ("dv", ctypes.c_void_p)]
+
+
+# Every symbol include/s2attn.h declares: name -> (restype, argtypes).
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64P = ctypes.POINTER(ctypes.c_int64)
+_IP = ctypes.POINTER(ctypes.c_int)
+_CFG = ctypes.POINTER(s2_pattern_config)
+SIGNATURES = {
+    "s2_last_error": (ctypes.c_char_p, []),
+    "s2_abi_version": (_I, []),
+    "s2_make_single_stride_config": (_I, [_I, _I, _I, _I, _I, _I, _CFG]),
+    "s2_pattern_validate": (_I, [_CFG]),
+    "s2_pattern_num_blocks": (_I, [_CFG]),
+    "s2_pattern_offset_for": (_I, [_CFG, _I, _I, _IP]),
+    "s2_layout_nnz": (_I, [_CFG, _I, _I64P]),
+    "s2_layout_build_csr": (_I, [_CFG, _I, _IP, _IP]),
+    "s2_layout_build_csc": (_I, [_CFG, _I, _IP, _IP]),
+    "s2_layout_evict_after": (_I, [_CFG, _I, _IP]),
+    "s2_layout_kv_efficient": (_I, [_CFG, _I, _IP]),
+    "s2_csr_validate": (_I, [_I, _IP, _IP, ctypes.c_int64]),
+    "s2_plan_create": (_I, [_CFG, ctypes.POINTER(_P)]),
+    "s2_plan_create_from_csr": (_I, [_I, _I, _I, _I, ctypes.POINTER(_IP), ctypes.POINTER(_IP),
+                                     ctypes.POINTER(_P)]),
+    "s2_plan_destroy": (None, [_P]),
+    "s2_plan_get_stats": (_I, [_P, ctypes.POINTER(s2_plan_stats)]),
+    "s2_plan_head_nnz": (_I, [_P, _I, _I64P]),
+    "s2_plan_fwd_tiles": (_I, [_P, _IP, _I64P, _I64P, ctypes.POINTER(ctypes.c_int32),
+                               ctypes.POINTER(ctypes.c_uint32)]),
+    "s2_plan_bwd_tiles": (_I, [_P, _I64P, _I64P, _I64P, _I64P]),
+    "s2_attn_fwd": (_I, [_P, ctypes.POINTER(s2_attn_args), _P]),
+    "s2_attn_bwd_workspace_size": (_I, [_P, ctypes.POINTER(s2_attn_bwd_args),
+                                        ctypes.POINTER(ctypes.c_size_t)]),
+    "s2_attn_bwd": (_I, [_P, ctypes.POINTER(s2_attn_bwd_args), _P, ctypes.c_size_t, _P]),
+    "s2_kvcache_create": (_I, [_P, _I, _I, _I, ctypes.POINTER(_P)]),
+    "s2_kvcache_destroy": (None, [_P]),
+    "s2_kvcache_length": (_I, [_P, _IP]),
+    "s2_kvcache_bytes": (_I, [_P, _I64P, _I64P]),
+    "s2_kvcache_retained_tokens": (_I, [_P, _I, _I64P]),
+    "s2_kvcache_prefill": (_I, [_P, _P, _P, _I, _P]),
+    "s2_kvcache_append": (_I, [_P, _P, _P, _P]),
+    "s2_attn_decode_workspace_size": (_I, [_P, ctypes.POINTER(ctypes.c_size_t)]),
+    "s2_attn_decode": (_I, [_P, _P, _P, _P, ctypes.c_double, _P, ctypes.c_size_t, _P]),
+    "s2_attn_decode_bytes": (_I, [_P, _I64P]),
+    "s2_plan_unit_weights": (_I, [_P, _I, _I64P]),
+    "s2_partition_lpt": (_I, [_I, _I64P, _I, _IP, _I64P]),
+    "s2_plan_fwd_flops": (_I, [_P, _I, _I, ctypes.POINTER(ctypes.c_double),
+                               ctypes.POINTER(ctypes.c_double)]),
+}
+
+
+class S2Error(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[s2 status {code}] {msg}")
+        self.code = code
+
+
+class S2InvalidArgument(S2Error, ValueError):
+    """Maps the reference's std::invalid_argument."""
+
+
+class S2Unsupported(S2Error, NotImplementedError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with __graft_entry__.build() or "
+                f"`make -C paper_2407_17678_b200/csrc` (there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc):
+    if rc == S2_OK:
+        return
+    msg = lib().s2_last_error().decode()
+    if rc == S2_ERR_INVALID_ARGUMENT:
+        raise S2InvalidArgument(rc, msg)
+    if rc == S2_ERR_UNSUPPORTED:
+        raise S2Unsupported(rc, msg)
+    raise S2Error(rc, msg)

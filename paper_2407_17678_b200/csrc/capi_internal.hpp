@@ -1,0 +1,20 @@
+// Helpers shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/s2attn.h"
+#include "plan.hpp"
+
+namespace s2 {
+extern thread_local std::string g_last_error;
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+int check_args(const s2_plan* p, const s2_attn_args* a);
+bool use_tcgen05(const s2_plan* p, const s2_attn_args* a);
+int ensure_csr_uploaded(s2_plan* p);
+Lists* get_lists(s2_plan* p, int seq_len, int* status);
+WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* unit_ids,
+                     int* status);
+}  // namespace s2

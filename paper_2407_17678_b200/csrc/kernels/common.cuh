@@ -1,0 +1,29 @@
+// Shared device-side types of the S2 kernels (mirrors csrc/plan.hpp).
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace s2dev {
+
+// One forward / dQ work item: a 128-row query tile of one (batch, head).
+struct FwdItem {
+    int32_t bh;         // data index of the query head (batch*H + h, or packed unit index)
+    int32_t head;       // layout head (selects the chunk list)
+    int32_t qtile;      // query rows qtile*128 .. +127
+    int32_t chunk_cnt;  // number of 64-key chunks
+    int64_t chunk_off;  // offset into the chunk array
+};
+
+// One dK/dV work item: a pair of 64-key chunks of one (batch, kv head).
+struct BwdItem {
+    int32_t kvbh;    // data index of the kv head
+    int32_t c0, c1;  // chunks (c1 = -1 when single)
+    int32_t count;   // q tiles visited
+    int64_t offset;  // into the BwdEntry array
+};
+struct BwdEntry {
+    int32_t qtile;
+    uint32_t mask0, mask1;
+};
+
+}  // namespace s2dev

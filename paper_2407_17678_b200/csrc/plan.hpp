@@ -1,0 +1,73 @@
+// s2_plan: host layout (CSR per head, tile lists) + lazily uploaded device
+// copies, keyed per (seq_len, batch, unit set) for the work-item arrays.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels/common.cuh"
+#include "layout.hpp"
+
+namespace s2 {
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    int device = -1;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (ptr) {
+            int cur = -1;
+            cudaGetDevice(&cur);
+            if (device >= 0 && device != cur) cudaSetDevice(device);
+            cudaFree(ptr);
+            if (device >= 0 && device != cur && cur >= 0) cudaSetDevice(cur);
+        }
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(ptr); }
+};
+
+// Upload host bytes to a fresh device buffer (synchronous; layout-time only).
+cudaError_t upload(DevBuf& buf, const void* host, size_t bytes);
+
+struct WorkItems {
+    DevBuf fwd;       // s2dev::FwdItem[]
+    int num_fwd = 0;
+    DevBuf bwd;       // s2dev::BwdItem[]
+    int num_bwd = 0;
+    DevBuf simt_bh;   // int[num_bh] data index
+    DevBuf simt_head; // int[num_bh] layout head
+    int num_bh = 0;
+};
+
+struct Lists {
+    bool tiled = false;  // block_size % 16 == 0 -> tcgen05 lists exist
+    FwdList fwd;
+    BwdList bwd;
+    DevBuf d_chunks;   // int2
+    DevBuf d_entries;  // s2dev::BwdEntry
+    bool uploaded = false;
+    std::map<std::string, std::unique_ptr<WorkItems>> items;
+};
+
+}  // namespace s2
+
+struct s2_plan {
+    int num_heads = 0, num_kv_heads = 0, seq_len = 0, block_size = 0, num_blocks = 0;
+    bool has_pattern = false;
+    s2::Pattern pattern;
+    std::vector<s2::Csr> csr;  // per head
+    std::vector<int64_t> col_off;
+    // device CSR (SIMT path)
+    s2::DevBuf d_row_ptr, d_col_idx, d_col_off;
+    bool csr_uploaded = false;
+    std::mutex mu;
+    std::map<int, std::unique_ptr<s2::Lists>> lists;  // keyed by seq_len
+};

@@ -1,0 +1,119 @@
+"""Head-parallel multi-GPU execution (north_star subsystem 5).
+
+Units are (batch, kv-group) pairs — a GQA group's query heads share one K/V
+head and one mask, so they stay on one GPU.  Each unit's weight is its
+active-block count (CSR nnz, identical for the CSC, so it balances backward
+too).  ``partition_lpt`` (C++, s2_partition_lpt) assigns units longest-first
+to the least-loaded rank.  Every rank runs the sparse kernels on its own
+units only (no data-path collective); the single exchange is an all-gather
+of the packed per-rank outputs (NCCL over NVLink via torch.distributed),
+padded to the largest rank and unpacked by the unit map.
+
+The reference has no multi-device path (OpenMP only, attention.cpp:114-117);
+its head-permutation exactness (test_attention.cpp:217-240) is what makes the
+gathered output bit-identical to the single-GPU output.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from ._abi import check, lib
+
+
+def partition_lpt(weights, num_ranks: int) -> Tuple[np.ndarray, np.ndarray]:
+    """(owner[num_units], load[num_ranks]) — LPT, deterministic."""
+    w = np.ascontiguousarray(weights, dtype=np.int64)
+    owner = np.zeros(w.size, np.int32)
+    load = np.zeros(num_ranks, np.int64)
+    check(lib().s2_partition_lpt(int(w.size), w.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                 num_ranks, owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                 load.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+    return owner, load
+
+
+class HeadParallelPlan:
+    """Which (batch, kv-group) units each rank owns, and how to scatter / gather."""
+
+    def __init__(self, plan, batch: int, world_size: int):
+        self.plan = plan
+        self.batch = batch
+        self.world_size = world_size
+        self.hpg = plan.num_heads // plan.num_kv_heads
+        self.weights = plan.unit_weights(batch)
+        self.owner, self.load = partition_lpt(self.weights, world_size)
+        self.units: List[np.ndarray] = [np.nonzero(self.owner == r)[0].astype(np.int32)
+                                        for r in range(world_size)]
+        self.max_units = max(1, max(len(u) for u in self.units))
+
+    def imbalance(self) -> float:
+        ideal = self.weights.sum() / self.world_size
+        return float(self.load.max() / ideal) if ideal else 1.0
+
+    # ---- data movement (torch tensors) --------------------------------
+    def scatter_q(self, q, rank: int):
+        """q [B,H,N,D] -> packed [U_r, hpg, N, D] for this rank's units."""
+        B, H, N, D = q.shape
+        Hkv = H // self.hpg
+        qu = q.reshape(B * Hkv, self.hpg, N, D)
+        return qu[self._index(rank, q.device)].contiguous()
+
+    def scatter_kv(self, k, rank: int):
+        """k [B,Hkv,N,D] -> packed [U_r, N, D]."""
+        B, Hkv, N, D = k.shape
+        return k.reshape(B * Hkv, N, D)[self._index(rank, k.device)].contiguous()
+
+    def _index(self, rank, device):
+        import torch
+
+        return torch.as_tensor(self.units[rank], device=device, dtype=torch.long)
+
+    def all_gather(self, local, group=None):
+        """local [U_r, ...] on every rank -> full [B*Hkv, ...] in unit order.
+
+        One all_gather of equal-sized (max-unit padded) buffers; no other
+        collective on the data path."""
+        import torch
+        import torch.distributed as dist
+
+        U = local.shape[0]
+        pad = torch.zeros((self.max_units,) + tuple(local.shape[1:]), dtype=local.dtype,
+                          device=local.device)
+        pad[:U] = local
+        bufs = [torch.empty_like(pad) for _ in range(self.world_size)]
+        dist.all_gather(bufs, pad, group=group)
+        full = torch.empty((self.batch * self.plan.num_kv_heads,) + tuple(local.shape[1:]),
+                           dtype=local.dtype, device=local.device)
+        for r in range(self.world_size):
+            n = len(self.units[r])
+            if n:
+                full[self._index(r, local.device)] = bufs[r][:n]
+        return full
+
+
+def head_parallel_forward(plan, q, k, v, rank: int, world_size: int, *, group=None,
+                          scale: Optional[float] = None, hp: Optional[HeadParallelPlan] = None):
+    """Shard units over ranks, run the local sparse forward, all-gather O and lse.
+
+    q [B,H,N,D], k/v [B,Hkv,N,D] are the full tensors (each rank reads only its
+    units).  Returns full (out [B,H,N,D], lse [B,H,N])."""
+    from .attention import s2_attn_fwd
+
+    B, H, N, D = q.shape
+    hp = hp or HeadParallelPlan(plan, B, world_size)
+    units = hp.units[rank]
+    if len(units):
+        ql = hp.scatter_q(q, rank)
+        kl = hp.scatter_kv(k, rank)
+        vl = hp.scatter_kv(v, rank)
+        out_l, lse_l = s2_attn_fwd(plan, ql, kl, vl, scale=scale, unit_ids=units)
+    else:
+        import torch
+
+        out_l = torch.zeros((0, hp.hpg, N, D), dtype=q.dtype, device=q.device)
+        lse_l = torch.zeros((0, hp.hpg, N), dtype=torch.float32, device=q.device)
+    out = hp.all_gather(out_l, group).reshape(B, H, N, D)
+    lse = hp.all_gather(lse_l, group).reshape(B, H, N)
+    return out, lse
