@@ -12,9 +12,9 @@
 #include "tma_host.hpp"
 
 cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtensorMap& k,
-                                const CUtensorMap& v, const s2dev::FwdItem* items, int num_items,
-                                const int2* chunks, __nv_bfloat16* out, float* lse, int seq_len,
-                                int hpg, float scale_log2, cudaStream_t stream);
+                                const CUtensorMap& v, const void* items, int num_items,
+                                const void* steps, __nv_bfloat16* out, float* lse, int seq_len,
+                                int hpg, float scale_log2, int num_sms, cudaStream_t stream);
 cudaError_t s2_launch_fwd_simt(bool bf16, const void* q, const void* k, const void* v, void* out,
                                float* lse, const int* bh_list, const int* head_of, int num_bh,
                                const int* row_ptr, const int* col_idx, const int64_t* col_off,
@@ -92,6 +92,7 @@ Lists* get_lists(s2_plan* p, int seq_len, int* status) {
         nl->tiled = p->block_size % 16 == 0;
         if (nl->tiled) {
             nl->fwd = build_fwd_list(p->csr, seq_len, p->block_size);
+            nl->pairs = build_pair_list(nl->fwd, p->num_heads);
             nl->bwd = build_bwd_list(nl->fwd, p->num_heads, p->num_kv_heads, seq_len);
         }
         L = nl.get();
@@ -103,7 +104,10 @@ Lists* get_lists(s2_plan* p, int seq_len, int* status) {
         static_assert(sizeof(ChunkEntry) == 8, "ChunkEntry layout");
         static_assert(sizeof(BwdEntry) == sizeof(s2dev::BwdEntry), "BwdEntry layout");
         cudaError_t e;
+        static_assert(sizeof(PairStep) == 24, "PairStep layout");
         if ((e = upload(L->d_chunks, L->fwd.chunks.data(), L->fwd.chunks.size() * 8)) != cudaSuccess ||
+            (e = upload(L->d_steps, L->pairs.steps.data(), L->pairs.steps.size() * sizeof(PairStep))) !=
+                cudaSuccess ||
             (e = upload(L->d_entries, L->bwd.entries.data(),
                         L->bwd.entries.size() * sizeof(BwdEntry))) != cudaSuccess) {
             *status = cuda_fail(e, "uploading tile lists");
@@ -165,6 +169,27 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
         std::stable_sort(fi.begin(), fi.end(), [](const s2dev::FwdItem& a, const s2dev::FwdItem& b) {
             return a.chunk_cnt > b.chunk_cnt;
         });
+        struct PairItem {
+            int32_t bh, qpair, nsteps, has_b;
+            int64_t step_off;
+        };
+        std::vector<PairItem> pi;
+        const int np = L->pairs.num_pairs;
+        for (size_t i = 0; i < bh.size(); ++i)
+            for (int q = 0; q < np; ++q) {
+                const size_t w_ = static_cast<size_t>(head[i]) * np + q;
+                const int64_t off = L->pairs.offset[w_];
+                pi.push_back({bh[i], q, static_cast<int32_t>(L->pairs.offset[w_ + 1] - off),
+                              2 * q + 1 < nt ? 1 : 0, off});
+            }
+        std::stable_sort(pi.begin(), pi.end(), [](const PairItem& a, const PairItem& b) {
+            return a.nsteps * (1 + a.has_b) > b.nsteps * (1 + b.has_b);
+        });
+        w->num_pair = static_cast<int>(pi.size());
+        if ((e = upload(w->pair, pi.data(), pi.size() * sizeof(PairItem))) != cudaSuccess) {
+            *status = cuda_fail(e, "uploading work items");
+            return nullptr;
+        }
         std::vector<s2dev::BwdItem> bi;
         for (size_t ui = 0; ui < units.size(); ++ui) {
             const int g = units[ui] % p->num_kv_heads;
@@ -215,6 +240,13 @@ int check_args(const s2_plan* p, const s2_attn_args* a) {
                 return fail(S2_ERR_INVALID_ARGUMENT, "unit id outside [0, batch*num_kv_heads)");
     }
     return S2_OK;
+}
+
+int num_sms() {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
 }
 
 bool use_tcgen05(const s2_plan* p, const s2_attn_args* a) {
@@ -552,9 +584,9 @@ int s2_attn_fwd(s2_plan* p, const s2_attn_args* a, s2_stream_t stream) {
             const CUtensorMap mq = s2host::make_map_bf16_3d(a->q, D, N, uint64_t(nu) * hpg, 64, 128);
             const CUtensorMap mk = s2host::make_map_bf16_3d(a->k, D, N, nu, 64, 64);
             const CUtensorMap mv = s2host::make_map_bf16_3d(a->v, D, N, nu, 64, 64);
-            e = s2_launch_fwd_sm100(a->head_dim, mq, mk, mv, w->fwd.as<s2dev::FwdItem>(), w->num_fwd,
-                                    L->d_chunks.as<int2>(), static_cast<__nv_bfloat16*>(a->out),
-                                    a->lse, a->seq_len, hpg, float(scale * M_LOG2E), st);
+            e = s2_launch_fwd_sm100(a->head_dim, mq, mk, mv, w->pair.ptr, w->num_pair,
+                                    L->d_steps.ptr, static_cast<__nv_bfloat16*>(a->out), a->lse,
+                                    a->seq_len, hpg, float(scale * M_LOG2E), num_sms(), st);
         } catch (const std::exception& ex) {
             return fail(S2_ERR_CUDA, ex.what());
         }

@@ -12,6 +12,7 @@ extern thread_local std::string g_last_error;
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 int check_args(const s2_plan* p, const s2_attn_args* a);
+int num_sms();
 bool use_tcgen05(const s2_plan* p, const s2_attn_args* a);
 int ensure_csr_uploaded(s2_plan* p);
 Lists* get_lists(s2_plan* p, int seq_len, int* status);

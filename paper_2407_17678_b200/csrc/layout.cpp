@@ -207,6 +207,49 @@ FwdList build_fwd_list(const std::vector<Csr>& csr, int seq_len, int block_size)
     return f;
 }
 
+PairList build_pair_list(const FwdList& fwd, int num_heads) {
+    PairList pl;
+    pl.num_pairs = (fwd.num_qtiles + 1) / 2;
+    pl.offset.assign(static_cast<size_t>(num_heads) * pl.num_pairs + 1, 0);
+    struct U {
+        int32_t c;
+        uint32_t a, b;
+    };
+    std::vector<U> uni;
+    for (int h = 0; h < num_heads; ++h)
+        for (int p = 0; p < pl.num_pairs; ++p) {
+            uni.clear();
+            const size_t wa = static_cast<size_t>(h) * fwd.num_qtiles + 2 * p;
+            const bool has_b = 2 * p + 1 < fwd.num_qtiles;
+            int64_t ia = fwd.offset[wa], ea = fwd.offset[wa + 1];
+            int64_t ib = has_b ? fwd.offset[wa + 1] : 0, eb = has_b ? fwd.offset[wa + 2] : 0;
+            while (ia < ea || ib < eb) {
+                if (ib >= eb || (ia < ea && fwd.chunks[ia].chunk < fwd.chunks[ib].chunk)) {
+                    uni.push_back({fwd.chunks[ia].chunk, fwd.chunks[ia].mask, 0u});
+                    ++ia;
+                } else if (ia >= ea || fwd.chunks[ib].chunk < fwd.chunks[ia].chunk) {
+                    uni.push_back({fwd.chunks[ib].chunk, 0u, fwd.chunks[ib].mask});
+                    ++ib;
+                } else {
+                    uni.push_back({fwd.chunks[ia].chunk, fwd.chunks[ia].mask, fwd.chunks[ib].mask});
+                    ++ia;
+                    ++ib;
+                }
+            }
+            for (size_t i = 0; i < uni.size(); i += 2) {
+                PairStep s{uni[i].c, -1, uni[i].a, 0u, uni[i].b, 0u};
+                if (i + 1 < uni.size()) {
+                    s.c1 = uni[i + 1].c;
+                    s.a1 = uni[i + 1].a;
+                    s.b1 = uni[i + 1].b;
+                }
+                pl.steps.push_back(s);
+            }
+            pl.offset[static_cast<size_t>(h) * pl.num_pairs + p + 1] = static_cast<int64_t>(pl.steps.size());
+        }
+    return pl;
+}
+
 BwdList build_bwd_list(const FwdList& fwd, int num_heads, int num_kv_heads, int seq_len) {
     BwdList b;
     const int hpg = num_heads / num_kv_heads;

@@ -79,6 +79,21 @@ struct FwdList {
 };
 FwdList build_fwd_list(const std::vector<Csr>& csr, int seq_len, int block_size);
 
+// Forward / dQ steps for a PAIR of adjacent query tiles (2p, 2p+1) sharing
+// every K/V load: the union of both tiles' chunk lists, two chunks per step,
+// with each tile's masks (0 = the tile skips that chunk).
+struct PairStep {
+    int32_t c0, c1;      // chunks (c1 = -1 when the step holds one chunk)
+    uint32_t a0, a1;     // tile 2p   masks for c0 / c1
+    uint32_t b0, b1;     // tile 2p+1 masks for c0 / c1
+};
+struct PairList {
+    int num_pairs = 0;
+    std::vector<int64_t> offset;  // [H * num_pairs + 1]
+    std::vector<PairStep> steps;
+};
+PairList build_pair_list(const FwdList& fwd, int num_heads);
+
 // dK/dV: per (kv group, key tile) a pair of chunks (c1 may be -1) and the
 // ascending list of q tiles with the two chunk masks.  Chunks of one group
 // are paired by similarity of their q-tile lists so stripe blocks pair with

@@ -38,8 +38,10 @@ struct DevBuf {
 cudaError_t upload(DevBuf& buf, const void* host, size_t bytes);
 
 struct WorkItems {
-    DevBuf fwd;       // s2dev::FwdItem[]
+    DevBuf fwd;       // s2dev::FwdItem[] (per 128-row q tile; dQ kernel)
     int num_fwd = 0;
+    DevBuf pair;      // PairItem[] (per q-tile pair; forward kernel)
+    int num_pair = 0;
     DevBuf bwd;       // s2dev::BwdItem[]
     int num_bwd = 0;
     DevBuf simt_bh;   // int[num_bh] data index
@@ -50,8 +52,10 @@ struct WorkItems {
 struct Lists {
     bool tiled = false;  // block_size % 16 == 0 -> tcgen05 lists exist
     FwdList fwd;
+    PairList pairs;
     BwdList bwd;
     DevBuf d_chunks;   // int2
+    DevBuf d_steps;    // PairStep
     DevBuf d_entries;  // s2dev::BwdEntry
     bool uploaded = false;
     std::map<std::string, std::unique_ptr<WorkItems>> items;
