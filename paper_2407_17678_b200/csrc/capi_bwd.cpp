@@ -1,16 +1,95 @@
 // C ABI: backward (dQ over the CSR tile list, dK/dV over the transposed list).
+#include <cmath>
+
 #include "capi_internal.hpp"
+#include "tma_host.hpp"
+
+cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* dout,
+                               const float* lse, float* delta, float* lse2, int num_bh, int N,
+                               int Npad, int D, cudaStream_t stream);
+cudaError_t s2_launch_bwd_sm100(int D, const CUtensorMap& q64, const CUtensorMap& do64,
+                                const CUtensorMap& q128, const CUtensorMap& do128,
+                                const CUtensorMap& k, const CUtensorMap& v, const void* dkv_items,
+                                int num_dkv, const void* dkv_entries, const void* dq_items,
+                                int num_dq, const void* dq_chunks, const float* lse2,
+                                const float* delta, __nv_bfloat16* dq, __nv_bfloat16* dk,
+                                __nv_bfloat16* dv, int N, int Npad, int hpg, float scale,
+                                int num_sms, cudaStream_t stream);
 
 using namespace s2;
+
+namespace {
+int num_q_heads(const s2_plan* p, const s2_attn_args* a) {
+    const int hpg = p->num_heads / p->num_kv_heads;
+    return (a->unit_ids ? a->num_units : a->batch * p->num_kv_heads) * hpg;
+}
+size_t ws_bytes(const s2_plan* p, const s2_attn_args* a) {
+    const size_t npad = (static_cast<size_t>(a->seq_len) + 127) / 128 * 128;
+    return 2 * static_cast<size_t>(num_q_heads(p, a)) * npad * sizeof(float);
+}
+int check_bwd(const s2_plan* p, const s2_attn_bwd_args* a) {
+    if (!a) return fail(S2_ERR_INVALID_ARGUMENT, "args is null");
+    if (int rc = check_args(p, &a->fwd)) return rc;
+    if (!a->dout || !a->dq || !a->dk || !a->dv)
+        return fail(S2_ERR_INVALID_ARGUMENT, "dout/dq/dk/dv must be non-null device pointers");
+    if (!use_tcgen05(p, &a->fwd))
+        return fail(S2_ERR_UNSUPPORTED,
+                    "backward needs bf16, head_dim in {64,128} and block_size % 16 == 0");
+    return S2_OK;
+}
+}  // namespace
 
 extern "C" {
 int s2_attn_bwd_workspace_size(const s2_plan* p, const s2_attn_bwd_args* a, size_t* bytes) {
     if (!bytes) return fail(S2_ERR_INVALID_ARGUMENT, "null argument");
-    if (int rc = check_args(p, a ? &a->fwd : nullptr)) return rc;
-    *bytes = 0;
+    if (int rc = check_bwd(p, a)) return rc;
+    *bytes = ws_bytes(p, &a->fwd);
     return S2_OK;
 }
-int s2_attn_bwd(s2_plan*, const s2_attn_bwd_args*, void*, size_t, s2_stream_t) {
-    return fail(S2_ERR_UNSUPPORTED, "backward not built yet");
+
+int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t workspace_bytes,
+                s2_stream_t stream) {
+    if (int rc = check_bwd(p, a)) return rc;
+    const s2_attn_args& f = a->fwd;
+    if (workspace_bytes < ws_bytes(p, &f) || !workspace)
+        return fail(S2_ERR_INVALID_ARGUMENT, "workspace too small (s2_attn_bwd_workspace_size)");
+    std::lock_guard<std::mutex> lk(p->mu);
+    int rc = S2_OK;
+    Lists* L = get_lists(p, f.seq_len, &rc);
+    if (!L) return rc;
+    WorkItems* w = get_items(p, L, f.batch, f.num_units, f.unit_ids, &rc);
+    if (!w) return rc;
+    const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int hpg = p->num_heads / p->num_kv_heads;
+    const int nqbh = num_q_heads(p, &f);
+    const int nkv = nqbh / hpg;
+    const int N = f.seq_len, D = f.head_dim;
+    const int Npad = (N + 127) / 128 * 128;
+    const double scale = f.scale != 0.0 ? f.scale : 1.0 / std::sqrt(double(D));
+    float* delta = static_cast<float*>(workspace);
+    float* lse2 = delta + static_cast<size_t>(nqbh) * Npad;
+    cudaError_t e = s2_launch_bwd_prep(static_cast<const __nv_bfloat16*>(f.out),
+                                       static_cast<const __nv_bfloat16*>(a->dout), f.lse, delta,
+                                       lse2, nqbh, N, Npad, D, st);
+    if (e != cudaSuccess) return cuda_fail(e, "s2_attn_bwd prep launch");
+    try {
+        using s2host::make_map_bf16_3d;
+        const CUtensorMap q64 = make_map_bf16_3d(f.q, D, N, nqbh, 64, 64);
+        const CUtensorMap do64 = make_map_bf16_3d(a->dout, D, N, nqbh, 64, 64);
+        const CUtensorMap q128 = make_map_bf16_3d(f.q, D, N, nqbh, 64, 128);
+        const CUtensorMap do128 = make_map_bf16_3d(a->dout, D, N, nqbh, 64, 128);
+        const CUtensorMap mk = make_map_bf16_3d(f.k, D, N, nkv, 64, 64);
+        const CUtensorMap mv = make_map_bf16_3d(f.v, D, N, nkv, 64, 64);
+        e = s2_launch_bwd_sm100(D, q64, do64, q128, do128, mk, mv, w->bwd.ptr, w->num_bwd,
+                                L->d_entries.ptr, w->fwd.ptr, w->num_fwd, L->d_chunks.ptr, lse2,
+                                delta, static_cast<__nv_bfloat16*>(a->dq),
+                                static_cast<__nv_bfloat16*>(a->dk),
+                                static_cast<__nv_bfloat16*>(a->dv), N, Npad, hpg, float(scale),
+                                num_sms(), st);
+    } catch (const std::exception& ex) {
+        return fail(S2_ERR_CUDA, ex.what());
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "s2_attn_bwd launch");
+    return S2_OK;
 }
 }

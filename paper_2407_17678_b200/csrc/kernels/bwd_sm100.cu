@@ -1,0 +1,587 @@
+// S2-Attention backward, sm_100a (no reference symbol: SPEC.md:262).
+//
+// Gradient of out = softmax_masked(scale * Q K^T) V over the same admitted
+// set as the forward (reference.cpp:28-36): P = exp(scale*S - lse),
+// dP = dO V^T, dS = P o (dP - Delta), Delta = rowsum(dO o O),
+// dV = P^T dO, dK = scale * dS^T Q, dQ = scale * dS K.
+//
+//  * s2_bwd_prep_kernel: Delta and lse*log2(e) into row-padded workspaces.
+//  * s2_bwd_dkv_kernel:  one CTA owns a 128-key tile (two 64-key chunks,
+//    paired by similar q-tile lists) of one kv head and walks the TRANSPOSED
+//    tile list (every q tile of every query head of its GQA group that
+//    attends it) in 64-row halves.  dK/dV accumulate in TMEM and are written
+//    once: no atomics, deterministic.
+//  * s2_bwd_dq_kernel:   one CTA owns a 128-row query tile and walks its
+//    CSR chunk list, dQ accumulating in TMEM.
+//
+// Both use the same warp layout (384 threads): warp 0 TMA producer, warp 1
+// MMA issuer, warp 2 TMEM allocator, warps 4-7 / 8-11 two elementwise
+// warpgroups that split the 64 columns of each score tile (32 each), with
+// S/dP double-buffered in TMEM so the elementwise pass of step n overlaps
+// the MMAs of steps n-1 and n+1.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace s2dev {
+
+// ------------------------------------------------------------------ prep
+__global__ void __launch_bounds__(256) s2_bwd_prep_kernel(const __nv_bfloat16* __restrict__ out,
+                                                          const __nv_bfloat16* __restrict__ dout,
+                                                          const float* __restrict__ lse,
+                                                          float* __restrict__ delta,
+                                                          float* __restrict__ lse2, int num_bh,
+                                                          int N, int Npad, int D) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long total = static_cast<long long>(num_bh) * Npad;
+    if (warp >= total) return;
+    const int bh = static_cast<int>(warp / Npad), row = static_cast<int>(warp % Npad);
+    float acc = 0.f;
+    if (row < N) {
+        const __nv_bfloat16* o = out + (static_cast<size_t>(bh) * N + row) * D;
+        const __nv_bfloat16* g = dout + (static_cast<size_t>(bh) * N + row) * D;
+        for (int x = lane * 2; x < D; x += 64) {
+            const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(o + x);
+            const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(g + x);
+            acc = fmaf(__low2float(a), __low2float(b), acc);
+            acc = fmaf(__high2float(a), __high2float(b), acc);
+        }
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+    if (lane == 0) {
+        delta[warp] = acc;
+        lse2[warp] = row < N ? lse[static_cast<size_t>(bh) * N + row] * 1.4426950408889634f : INFINITY;
+    }
+}
+
+struct BwdParams {
+    const void* items;
+    int num_items;
+    const void* entries;  // BwdEntry (dkv) or int2 chunks (dq)
+    const float* lse2;    // [num_qbh][Npad], log2 domain, +inf padding
+    const float* delta;   // [num_qbh][Npad]
+    __nv_bfloat16* g0;    // dkv: dK ; dq: dQ
+    __nv_bfloat16* g1;    // dkv: dV
+    int N, Npad, hpg;
+    float scale_log2, scale;
+};
+
+template <int D>
+struct BwdCfg {
+    static constexpr int kSub = D / 64;
+    static constexpr int kTile128 = kSub * 16384;  // 128 rows x D bf16
+    static constexpr int kTile64 = kSub * 8192;    // 64 rows x D bf16
+    static constexpr int kNST = 4;
+    // dkv: resident K, V (128 keys); stages: Q64, dO64, lse2[64], delta[64]
+    static constexpr int kDkvStage = 2 * kTile64 + 512;
+    static constexpr int kDkvSmem = 1024 + 2 * kTile128 + kNST * kDkvStage;
+    // dq: resident Q, dO (128 rows); stages: K64, V64
+    static constexpr int kDqStage = 2 * kTile64;
+    static constexpr int kDqSmem = 1024 + 2 * kTile128 + kNST * kDqStage;
+};
+
+// Number of (head, entry, half) steps of a dK/dV item: a 64-row half is
+// skipped when neither chunk mask has a bit in its four row groups.
+__device__ __forceinline__ bool half_active(const BwdEntry& e, int half) {
+    return (((e.mask0 | e.mask1) >> (16 * half)) & 0xFFFFu) != 0;
+}
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    s2_bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
+                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                      const BwdParams p) {
+    using C = BwdCfg<D>;
+    constexpr int NST = C::kNST;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar_kvf, bar_kve, bar_sf[NST], bar_se[NST], bar_s[2], bar_p[2], bar_af, bar_ae;
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sK = smem_u32(smem), sV = sK + C::kTile128;
+    const uint32_t sSt = sV + C::kTile128;
+    const BwdItem* items = static_cast<const BwdItem*>(p.items);
+    const BwdEntry* ents = static_cast<const BwdEntry*>(p.entries);
+
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar_kvf), 1);
+        mbar_init(smem_u32(&bar_kve), 1);
+        mbar_init(smem_u32(&bar_af), 1);
+        mbar_init(smem_u32(&bar_ae), 256);
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(smem_u32(&bar_sf[i]), 1);
+            mbar_init(smem_u32(&bar_se[i]), 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&bar_s[i]), 1);
+            mbar_init(smem_u32(&bar_p[i]), 256);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) {
+        tmem_alloc(smem_u32(&tmem_base_s), 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    // TMEM: S^T[b] at 64b, dP^T[b] at 128+64b, dV at 256, dK at 384.
+
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+        if (warp == 0 && lane == 0) {
+            // ---------------------------------------------------- producer
+            tma_prefetch(&tmQ);
+            tma_prefetch(&tmdO);
+            tma_prefetch(&tmK);
+            tma_prefetch(&tmV);
+            uint32_t it_cnt = 0, st_it = 0;
+            for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+                const BwdItem it = items[i];
+                if (it_cnt > 0) mbar_wait(smem_u32(&bar_kve), (it_cnt - 1) & 1);
+                const int nc = it.c1 >= 0 ? 2 : 1;
+                mbar_expect_tx(smem_u32(&bar_kvf), 2 * nc * C::kSub * 8192);
+                for (int h = 0; h < nc; ++h)
+                    for (int s = 0; s < C::kSub; ++s) {
+                        const int row = (h ? it.c1 : it.c0) * 64;
+                        tma_load_3d(sK + s * 16384 + h * 8192, &tmK, smem_u32(&bar_kvf), s * 64, row, it.kvbh);
+                        tma_load_3d(sV + s * 16384 + h * 8192, &tmV, smem_u32(&bar_kvf), s * 64, row, it.kvbh);
+                    }
+                for (int j = 0; j < p.hpg; ++j) {
+                    const int qbh = it.kvbh * p.hpg + j;
+                    for (int e = 0; e < it.count; ++e) {
+                        const BwdEntry en = ents[it.offset + e];
+                        for (int half = 0; half < 2; ++half) {
+                            if (!half_active(en, half)) continue;
+                            const int st = st_it % NST;
+                            if (st_it >= NST) mbar_wait(smem_u32(&bar_se[st]), ((st_it / NST) + 1) & 1);
+                            const uint32_t base = sSt + st * C::kDkvStage;
+                            const uint32_t bar = smem_u32(&bar_sf[st]);
+                            const int row0 = en.qtile * 128 + half * 64;
+                            mbar_expect_tx(bar, 2 * C::kTile64 + 512);
+                            for (int s = 0; s < C::kSub; ++s) {
+                                tma_load_3d(base + s * 8192, &tmQ, bar, s * 64, row0, qbh);
+                                tma_load_3d(base + C::kTile64 + s * 8192, &tmdO, bar, s * 64, row0, qbh);
+                            }
+                            const size_t lo = static_cast<size_t>(qbh) * p.Npad + row0;
+                            bulk_load(base + 2 * C::kTile64, p.lse2 + lo, 256, bar);
+                            bulk_load(base + 2 * C::kTile64 + 256, p.delta + lo, 256, bar);
+                            ++st_it;
+                        }
+                    }
+                }
+            }
+        } else if (warp == 1 && lane == 0) {
+            // ---------------------------------------------------- MMA issuer
+            constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);
+            constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
+            uint32_t it_cnt = 0, st_it = 0, n_glob = 0;
+            for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+                const BwdItem it = items[i];
+                mbar_wait(smem_u32(&bar_kvf), it_cnt & 1);
+                tc_fence_after();
+                bool first = true;
+                int prev_st = -1;
+                uint32_t prev_n = 0;
+                auto accumulate = [&](uint32_t n, int st) {
+                    const int b = n & 1;
+                    mbar_wait(smem_u32(&bar_p[b]), (n >> 1) & 1);
+                    if (first && it_cnt > 0) mbar_wait(smem_u32(&bar_ae), (it_cnt - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t base = sSt + st * C::kDkvStage;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+                        // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
+                        mma_ts(tmem + 256, tmem + b * 64 + kk * 8,
+                               umma_desc_sw128(base + C::kTile64 + kk * 2048, 8192, 1024), idA, acc);
+                        mma_ts(tmem + 384, tmem + 128 + b * 64 + kk * 8,
+                               umma_desc_sw128(base + kk * 2048, 8192, 1024), idA, acc);
+                    }
+                    first = false;
+                    mma_commit(smem_u32(&bar_se[st]));
+                };
+                for (int j = 0; j < p.hpg; ++j)
+                    for (int e = 0; e < it.count; ++e) {
+                        const BwdEntry en = ents[it.offset + e];
+                        for (int half = 0; half < 2; ++half) {
+                            if (!half_active(en, half)) continue;
+                            const int st = st_it % NST;
+                            mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
+                            tc_fence_after();
+                            const uint32_t base = sSt + st * C::kDkvStage;
+                            const int b = n_glob & 1;
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk) {
+                                const int sub = kk >> 2, off = (kk & 3) * 32;
+                                // S^T = K Q^T ; dP^T = V dO^T  (K-major x K-major)
+                                mma_ss(tmem + b * 64, umma_desc_sw128(sK + sub * 16384 + off, 16, 1024),
+                                       umma_desc_sw128(base + sub * 8192 + off, 16, 1024), idS, kk > 0);
+                                mma_ss(tmem + 128 + b * 64,
+                                       umma_desc_sw128(sV + sub * 16384 + off, 16, 1024),
+                                       umma_desc_sw128(base + C::kTile64 + sub * 8192 + off, 16, 1024),
+                                       idS, kk > 0);
+                            }
+                            mma_commit(smem_u32(&bar_s[b]));
+                            if (prev_st >= 0) accumulate(prev_n, prev_st);
+                            prev_st = st;
+                            prev_n = n_glob;
+                            ++n_glob;
+                            ++st_it;
+                        }
+                    }
+                if (prev_st >= 0) accumulate(prev_n, prev_st);
+                mma_commit(smem_u32(&bar_af));
+                mma_commit(smem_u32(&bar_kve));
+            }
+        }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+        // -------------------------------------------------------- elementwise
+        const int wg = (warp >> 2) - 1;  // column half of the 64 q columns
+        const int kr = tid & 127;         // key row == TMEM lane
+        const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const float sl2 = p.scale_log2;
+        uint32_t it_cnt = 0, st_it = 0, n_glob = 0;
+        for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+            const BwdItem it = items[i];
+            const int hk = kr >> 6;
+            const int chunk = hk ? it.c1 : it.c0;
+            const int cg = (kr & 63) >> 4;
+            const int key_pos = chunk * 64 + (kr & 63);
+            const bool key_ok = chunk >= 0 && key_pos < p.N;
+            for (int j = 0; j < p.hpg; ++j)
+                for (int e = 0; e < it.count; ++e) {
+                    const BwdEntry en = ents[it.offset + e];
+                    for (int half = 0; half < 2; ++half) {
+                        if (!half_active(en, half)) continue;
+                        const int st = st_it % NST;
+                        const int b = n_glob & 1;
+                        mbar_wait(smem_u32(&bar_s[b]), (n_glob >> 1) & 1);
+                        tc_fence_after();
+                        uint32_t su[32], du[32];
+                        tmem_ld32(tmem + b * 64 + wg * 32 + lane_off, su);
+                        tmem_ld32(tmem + 128 + b * 64 + wg * 32 + lane_off, du);
+                        const uint32_t m = key_ok ? (hk ? en.mask1 : en.mask0) : 0u;
+                        const float* sl = reinterpret_cast<const float*>(smem + (sSt - sK) + st * C::kDkvStage + 2 * C::kTile64);
+                        const int g0 = half * 4 + wg * 2;  // q row groups of my 32 columns
+                        const bool on0 = (m >> (g0 * 4 + cg)) & 1u;
+                        const bool on1 = (m >> ((g0 + 1) * 4 + cg)) & 1u;
+                        const int q0 = en.qtile * 128 + half * 64 + wg * 32;
+                        tmem_ld_wait();
+                        uint32_t pk[16], dk[16];
+#pragma unroll
+                        for (int c = 0; c < 32; c += 2) {
+                            float pv[2], dv[2];
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                const int cc = c + u;
+                                const bool ok = (cc < 16 ? on0 : on1) && key_pos <= q0 + cc;
+                                const float l2 = sl[wg * 32 + cc];
+                                const float dl = sl[64 + wg * 32 + cc];
+                                const float pe = fast_exp2(fmaf(__uint_as_float(su[cc]), sl2, -l2));
+                                pv[u] = ok ? pe : 0.f;
+                                dv[u] = ok ? pe * (__uint_as_float(du[cc]) - dl) : 0.f;
+                            }
+                            pk[c >> 1] = pack_bf16(pv[0], pv[1]);
+                            dk[c >> 1] = pack_bf16(dv[0], dv[1]);
+                        }
+                        tmem_st16(tmem + b * 64 + wg * 16 + lane_off, pk);
+                        tmem_st16(tmem + 128 + b * 64 + wg * 16 + lane_off, dk);
+                        tmem_st_wait();
+                        tc_fence_before();
+                        mbar_arrive(smem_u32(&bar_p[b]));
+                        ++n_glob;
+                        ++st_it;
+                    }
+                }
+            // ---------------------------------------------------- epilogue
+            mbar_wait(smem_u32(&bar_af), it_cnt & 1);
+            tc_fence_after();
+            const float mul = wg ? p.scale : 1.0f;  // wg0 -> dV, wg1 -> dK
+            __nv_bfloat16* dst = (wg ? p.g0 : p.g1) + (static_cast<size_t>(it.kvbh) * p.N + key_pos) * D;
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                uint32_t u[32];
+                tmem_ld32(tmem + (wg ? 384 : 256) + c * 32 + lane_off, u);
+                tmem_ld_wait();
+                if (key_ok) {
+                    uint4 w[4];
+                    uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        wp[q] = pack_bf16(__uint_as_float(u[2 * q]) * mul, __uint_as_float(u[2 * q + 1]) * mul);
+                    uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) d4[q] = w[q];
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(smem_u32(&bar_ae));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    s2_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
+                     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                     const BwdParams p) {
+    using C = BwdCfg<D>;
+    constexpr int NST = C::kNST;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar_qf, bar_qe, bar_sf[NST], bar_se[NST], bar_s[2], bar_p[2], bar_af, bar_ae;
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sQ = smem_u32(smem), sdO = sQ + C::kTile128;
+    const uint32_t sSt = sdO + C::kTile128;
+    const FwdItem* items = static_cast<const FwdItem*>(p.items);
+    const int2* chunks = static_cast<const int2*>(p.entries);
+
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar_qf), 1);
+        mbar_init(smem_u32(&bar_qe), 1);
+        mbar_init(smem_u32(&bar_af), 1);
+        mbar_init(smem_u32(&bar_ae), 256);
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(smem_u32(&bar_sf[i]), 1);
+            mbar_init(smem_u32(&bar_se[i]), 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&bar_s[i]), 1);
+            mbar_init(smem_u32(&bar_p[i]), 256);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) {
+        tmem_alloc(smem_u32(&tmem_base_s), 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    // TMEM: S[b] at 64b, dP[b] at 128+64b, dQ at 256.
+
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+        if (warp == 0 && lane == 0) {
+            tma_prefetch(&tmQ);
+            tma_prefetch(&tmdO);
+            tma_prefetch(&tmK);
+            tma_prefetch(&tmV);
+            const uint64_t keep = policy_evict_last();
+            uint32_t it_cnt = 0, st_it = 0;
+            for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+                const FwdItem it = items[i];
+                const int kvbh = it.bh / p.hpg;
+                if (it_cnt > 0) mbar_wait(smem_u32(&bar_qe), (it_cnt - 1) & 1);
+                mbar_expect_tx(smem_u32(&bar_qf), 2 * C::kTile128);
+                for (int s = 0; s < C::kSub; ++s) {
+                    tma_load_3d(sQ + s * 16384, &tmQ, smem_u32(&bar_qf), s * 64, it.qtile * 128, it.bh);
+                    tma_load_3d(sdO + s * 16384, &tmdO, smem_u32(&bar_qf), s * 64, it.qtile * 128, it.bh);
+                }
+                for (int n = 0; n < it.chunk_cnt; ++n, ++st_it) {
+                    const int st = st_it % NST;
+                    if (st_it >= NST) mbar_wait(smem_u32(&bar_se[st]), ((st_it / NST) + 1) & 1);
+                    const uint32_t base = sSt + st * C::kDqStage;
+                    const uint32_t bar = smem_u32(&bar_sf[st]);
+                    const int row = chunks[it.chunk_off + n].x * 64;
+                    mbar_expect_tx(bar, 2 * C::kTile64);
+                    for (int s = 0; s < C::kSub; ++s) {
+                        tma_load_3d_hint(base + s * 8192, &tmK, bar, s * 64, row, kvbh, keep);
+                        tma_load_3d_hint(base + C::kTile64 + s * 8192, &tmV, bar, s * 64, row, kvbh, keep);
+                    }
+                }
+            }
+        } else if (warp == 1 && lane == 0) {
+            constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);
+            constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
+            uint32_t it_cnt = 0, st_it = 0, n_glob = 0;
+            for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+                const FwdItem it = items[i];
+                mbar_wait(smem_u32(&bar_qf), it_cnt & 1);
+                tc_fence_after();
+                bool first = true;
+                auto accumulate = [&](uint32_t n, int st) {
+                    const int b = n & 1;
+                    mbar_wait(smem_u32(&bar_p[b]), (n >> 1) & 1);
+                    if (first && it_cnt > 0) mbar_wait(smem_u32(&bar_ae), (it_cnt - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t base = sSt + st * C::kDqStage;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)  // dQ += dS K  (K chunk as MN-major B)
+                        mma_ts(tmem + 256, tmem + 128 + b * 64 + kk * 8,
+                               umma_desc_sw128(base + kk * 2048, 8192, 1024), idA,
+                               (first && kk == 0) ? 0u : 1u);
+                    first = false;
+                    mma_commit(smem_u32(&bar_se[st]));
+                };
+                int prev_st = -1;
+                uint32_t prev_n = 0;
+                for (int n = 0; n < it.chunk_cnt; ++n, ++st_it, ++n_glob) {
+                    const int st = st_it % NST;
+                    mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
+                    tc_fence_after();
+                    const uint32_t base = sSt + st * C::kDqStage;
+                    const int b = n_glob & 1;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const int sub = kk >> 2, off = (kk & 3) * 32;
+                        mma_ss(tmem + b * 64, umma_desc_sw128(sQ + sub * 16384 + off, 16, 1024),
+                               umma_desc_sw128(base + sub * 8192 + off, 16, 1024), idS, kk > 0);
+                        mma_ss(tmem + 128 + b * 64, umma_desc_sw128(sdO + sub * 16384 + off, 16, 1024),
+                               umma_desc_sw128(base + C::kTile64 + sub * 8192 + off, 16, 1024), idS,
+                               kk > 0);
+                    }
+                    mma_commit(smem_u32(&bar_s[b]));
+                    if (prev_st >= 0) accumulate(prev_n, prev_st);
+                    prev_st = st;
+                    prev_n = n_glob;
+                }
+                if (prev_st >= 0) accumulate(prev_n, prev_st);
+                mma_commit(smem_u32(&bar_af));
+                mma_commit(smem_u32(&bar_qe));
+            }
+        }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+        const int wg = (warp >> 2) - 1;  // key-column half of each 64-key chunk
+        const int r = tid & 127;          // query row == TMEM lane
+        const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const float sl2 = p.scale_log2;
+        uint32_t it_cnt = 0, n_glob = 0;
+        for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+            const FwdItem it = items[i];
+            const int q_pos = it.qtile * 128 + r;
+            const size_t lrow = static_cast<size_t>(it.bh) * p.Npad + q_pos;
+            const float l2 = p.lse2[lrow];
+            const float dl = p.delta[lrow];
+            const int rg = r >> 4;
+            for (int n = 0; n < it.chunk_cnt; ++n, ++n_glob) {
+                const int2 ch = chunks[it.chunk_off + n];
+                const int b = n_glob & 1;
+                mbar_wait(smem_u32(&bar_s[b]), (n_glob >> 1) & 1);
+                tc_fence_after();
+                uint32_t su[32], du[32];
+                tmem_ld32(tmem + b * 64 + wg * 32 + lane_off, su);
+                tmem_ld32(tmem + 128 + b * 64 + wg * 32 + lane_off, du);
+                const uint32_t bits = (static_cast<uint32_t>(ch.y) >> (rg * 4)) & 0xFu;
+                const bool on0 = (bits >> (wg * 2)) & 1u, on1 = (bits >> (wg * 2 + 1)) & 1u;
+                const int k0 = ch.x * 64 + wg * 32;
+                tmem_ld_wait();
+                uint32_t dk[16];
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    float dv[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int cc = c + u;
+                        const bool ok = (cc < 16 ? on0 : on1) && k0 + cc <= q_pos;
+                        const float pe = fast_exp2(fmaf(__uint_as_float(su[cc]), sl2, -l2));
+                        dv[u] = ok ? pe * (__uint_as_float(du[cc]) - dl) : 0.f;
+                    }
+                    dk[c >> 1] = pack_bf16(dv[0], dv[1]);
+                }
+                tmem_st16(tmem + 128 + b * 64 + wg * 16 + lane_off, dk);
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(smem_u32(&bar_p[b]));
+            }
+            mbar_wait(smem_u32(&bar_af), it_cnt & 1);
+            tc_fence_after();
+            const bool valid = q_pos < p.N;
+            __nv_bfloat16* dst = p.g0 + (static_cast<size_t>(it.bh) * p.N + q_pos) * D + wg * (D / 2);
+#pragma unroll
+            for (int c = 0; c < D / 64; ++c) {
+                uint32_t u[32];
+                tmem_ld32(tmem + 256 + wg * (D / 2) + c * 32 + lane_off, u);
+                tmem_ld_wait();
+                if (valid) {
+                    uint4 w[4];
+                    uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        wp[q] = pack_bf16(__uint_as_float(u[2 * q]) * p.scale,
+                                          __uint_as_float(u[2 * q + 1]) * p.scale);
+                    uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) d4[q] = w[q];
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(smem_u32(&bar_ae));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+}  // namespace s2dev
+
+using namespace s2dev;
+
+cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* dout,
+                               const float* lse, float* delta, float* lse2, int num_bh, int N,
+                               int Npad, int D, cudaStream_t stream) {
+    const long long warps = static_cast<long long>(num_bh) * Npad;
+    const int blocks = static_cast<int>((warps * 32 + 255) / 256);
+    s2_bwd_prep_kernel<<<blocks, 256, 0, stream>>>(out, dout, lse, delta, lse2, num_bh, N, Npad, D);
+    return cudaGetLastError();
+}
+
+template <class K>
+static cudaError_t launch_bwd(K kern, int smem, int grid, const CUtensorMap& q,
+                              const CUtensorMap& dout, const CUtensorMap& k, const CUtensorMap& v,
+                              const BwdParams& p, cudaStream_t stream) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 384, smem, stream>>>(q, dout, k, v, p);
+    return cudaGetLastError();
+}
+
+// q64/do64: 64-row boxes (dkv); q128/do128: 128-row boxes (dq); k/v: 64-row boxes.
+cudaError_t s2_launch_bwd_sm100(int D, const CUtensorMap& q64, const CUtensorMap& do64,
+                                const CUtensorMap& q128, const CUtensorMap& do128,
+                                const CUtensorMap& k, const CUtensorMap& v, const void* dkv_items,
+                                int num_dkv, const void* dkv_entries, const void* dq_items,
+                                int num_dq, const void* dq_chunks, const float* lse2,
+                                const float* delta, __nv_bfloat16* dq, __nv_bfloat16* dk,
+                                __nv_bfloat16* dv, int N, int Npad, int hpg, float scale,
+                                int num_sms, cudaStream_t stream) {
+    const float sl2 = scale * 1.4426950408889634f;
+    BwdParams pk{dkv_items, num_dkv, dkv_entries, lse2, delta, dk, dv, N, Npad, hpg, sl2, scale};
+    BwdParams pq{dq_items, num_dq, dq_chunks, lse2, delta, dq, nullptr, N, Npad, hpg, sl2, scale};
+    const int gk = num_dkv < num_sms ? num_dkv : num_sms;
+    const int gq = num_dq < num_sms ? num_dq : num_sms;
+    cudaError_t e = cudaSuccess;
+    if (D == 128) {
+        if (num_dkv) e = launch_bwd(s2_bwd_dkv_kernel<128>, BwdCfg<128>::kDkvSmem, gk, q64, do64, k, v, pk, stream);
+        if (e == cudaSuccess && num_dq)
+            e = launch_bwd(s2_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmem, gq, q128, do128, k, v, pq, stream);
+    } else if (D == 64) {
+        if (num_dkv) e = launch_bwd(s2_bwd_dkv_kernel<64>, BwdCfg<64>::kDkvSmem, gk, q64, do64, k, v, pk, stream);
+        if (e == cudaSuccess && num_dq)
+            e = launch_bwd(s2_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmem, gq, q128, do128, k, v, pq, stream);
+    } else {
+        e = cudaErrorInvalidValue;
+    }
+    return e;
+}
