@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""bench.py — S2-Attention on B200 (BASELINE.json metric:
+"S2 attn fwd+bwd ms & active-block TFLOPS @32K; decode tok/s; vs CPU ref").
+
+A step = one S2 attention layer forward + backward over one batch of
+synthetic bf16 inputs at cfg3 (BASELINE.json configs[2]: S=32K, H=32, D=128,
+block 64, local_blocks 4, vert_stride 16, heterogeneous head offsets), per
+GPU.  Under torchrun (N>1) the (batch, head) units of a global batch of N are
+LPT-partitioned across ranks by active-block count (weak scaling) and the
+forward output is all-gathered with NCCL (the north_star's single exchange).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl s2|reference]
+
+value          whole-job active-block TFLOP/s of fwd+bwd (FLOPs_fwd = sum nnz *
+               4*D*64^2, analysis.cpp:29-31; FLOPs_bwd = 2.5 x FLOPs_fwd),
+               device time (CUDA events), max over ranks, inputs resident in HBM.
+e2e            the same through the public API with host buffers: H2D of q,k,v,dO
+               from pinned memory and D2H of out,lse,dq,dk,dv inside the timed region.
+roofline       dominant kernel of the step (CUDA events around every launch, via
+               s2_profile_*), algorithmic FLOPs / its average launch time.
+cpu_baseline   the reference's streaming_sharded_attention (oracle/_ref, built from
+               /root/reference) for the forward + the oracle's C restatement of the
+               backward (the reference has none), on a bounded sample of cfg3 heads.
+"""
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_SEQ, H, D, BLOCK, LOCAL, VSTRIDE = 32768, 32, 128, 64, 4, 16
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "fallback"
+
+
+def workload_cfg():
+    import paper_2407_17678_b200 as s2
+
+    return s2.make_s2_config(N_SEQ, H, block_size=BLOCK, local_blocks=LOCAL, vert_stride=VSTRIDE)
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- CPU side
+def cpu_sample(heads=(0,), seed=7):
+    """Time the reference CPU path on a bounded sample: fwd through the
+    reference library (or the port if it is absent), bwd through the port.
+    Returns (tflops, seconds, kind, sample_desc, flops)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle  # test/baseline infrastructure only
+
+    import paper_2407_17678_b200 as s2
+
+    cfg = workload_cfg()
+    ref = oracle.ref()
+    kind = "reference" if ref is not None else "port"
+    rng = np.random.default_rng(seed)
+    B = cfg.num_blocks()
+    tot_s = 0.0
+    flops = 0.0
+    for h in heads:
+        csr = s2.build_csr(cfg, h)
+        rp = np.ascontiguousarray(csr.row_ptr, np.int32)
+        ci = np.ascontiguousarray(csr.col_idx, np.int32)
+        n = N_SEQ * D
+        q, k, v, do = (rng.uniform(-1, 1, n).astype(np.float32) for _ in range(4))
+        out = np.zeros(n, np.float32)
+        lse = np.zeros(N_SEQ, np.float64)
+        t0 = time.perf_counter()
+        if ref is not None:
+            rc = ref.ref_streaming(1, N_SEQ, D, BLOCK, 0.0, oracle.fp(q), oracle.fp(k), oracle.fp(v),
+                                   B, oracle.ip(rp), oracle.ip(ci), 0, oracle.fp(out), oracle.dp(lse))
+            assert rc == 0
+        else:
+            oracle.attn_fwd(q, k, v, rp, ci, 1, 1, 1, N_SEQ, D, BLOCK)
+        oracle.attn_bwd(q, k, v, do, rp, ci, 1, 1, 1, N_SEQ, D, BLOCK)
+        tot_s += time.perf_counter() - t0
+        flops += 3.5 * csr.nnz() * 4.0 * D * BLOCK * BLOCK
+    desc = (f"cfg3 heads {list(heads)} of {H} (fwd: "
+            f"{'reference streaming_sharded_attention' if kind == 'reference' else 'oracle port'}"
+            f"; bwd: oracle C restatement, the reference has no backward), fp32/fp64, "
+            f"{host_cores()} threads")
+    return flops / tot_s / 1e12, tot_s, kind, desc, flops
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+    for _ in range(args.warmup):
+        cpu_sample(heads=(0,))
+    vals, secs = [], []
+    kind = desc = None
+    for i in range(args.steps):
+        v, s, kind, desc, _ = cpu_sample(heads=(i % H,))
+        vals.append(v)
+        secs.append(s)
+    value = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": "S2 attn fwd+bwd active-block TFLOP/s @32K",
+        "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * float(np.mean(secs)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config_desc(args.gpus),
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": host_cores(), "kind": kind,
+                         "sample": desc + "; one head per step"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_desc(n):
+    return {"workload": "cfg3: one S2 attention layer fwd+bwd, S=32768, H=32, D=128, block 64, "
+                        "local_blocks 4, vert_stride 16, heterogeneous head offsets",
+            "batch_per_gpu": 1, "global_batch": n, "seq_len": N_SEQ, "heads": H, "head_dim": D,
+            "parallelism": f"head-parallel x{n} (LPT by active blocks), all-gather of O",
+            "l2": "inputs 256 MiB per tensor > 126 MB L2; no flush needed"}
+
+
+# ------------------------------------------------------------- clock sampler
+class ClockSampler:
+    def __init__(self, dev_index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._h = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self._h = self._handle(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _handle(self, dev_index):
+        import torch
+
+        nv = self.nv
+        try:
+            uuid = str(torch.cuda.get_device_properties(dev_index).uuid)
+            for i in range(nv.nvmlDeviceGetCount()):
+                h = nv.nvmlDeviceGetHandleByIndex(i)
+                u = nv.nvmlDeviceGetUUID(h)
+                u = u.decode() if isinstance(u, bytes) else u
+                if uuid.replace("GPU-", "") in u:
+                    return h
+        except Exception:
+            pass
+        return nv.nvmlDeviceGetHandleByIndex(dev_index)
+
+    def _run(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------- GPU side
+def run_s2(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_17678_b200 as s2
+    from paper_2407_17678_b200 import _abi
+    from paper_2407_17678_b200.dist import HeadParallelPlan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = workload_cfg()
+    plan = s2.Plan.from_config(cfg)
+    hp = HeadParallelPlan(plan, world, world)  # global batch = world (weak scaling)
+    units = hp.units[rank]
+    U = len(units)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    mk = lambda: torch.rand((U, 1, N_SEQ, D), device=dev, generator=g, dtype=torch.float32)  # noqa
+    q, do = (mk().mul_(2).sub_(1).to(torch.bfloat16) for _ in range(2))
+    k, v = (mk().mul_(2).sub_(1).to(torch.bfloat16).reshape(U, N_SEQ, D) for _ in range(2))
+    out = torch.empty_like(q)
+    lse = torch.empty((U, 1, N_SEQ), device=dev, dtype=torch.float32)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    act1, dense1 = plan.fwd_flops(1, D)
+    # active FLOPs of this rank's units (per-unit weight = nnz of its head)
+    w = plan.unit_weights(world)
+    per_pair = 4.0 * D * BLOCK * BLOCK
+    my_fwd_flops = float(sum(w[u] for u in units)) * per_pair
+    tot_fwd_flops = float(w.sum()) * per_pair
+    dense_fwd_total = dense1 * world
+
+    def step():
+        s2.s2_attn_fwd(plan, q, k, v, out=out, lse=lse, unit_ids=units)
+        if world > 1:
+            hp.all_gather(out.reshape(U, 1, N_SEQ, D))
+        s2.s2_attn_bwd(plan, q, k, v, out, lse, do, dq=dq, dk=dk, dv=dv, unit_ids=units)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    lib = _abi.lib()
+    lib.s2_profile_enable(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    names = ctypes.create_string_buffer(32 * 16)
+    tot = (ctypes.c_double * 16)()
+    cnt = (ctypes.c_int * 16)()
+    nk = ctypes.c_int()
+    lib.s2_profile_collect(16, names, tot, cnt, ctypes.byref(nk))
+    lib.s2_profile_enable(0)
+    kernels = {}
+    for i in range(nk.value):
+        nm = names.raw[32 * i: 32 * i + 32].split(b"\0")[0].decode()
+        kernels[nm] = {"avg_ms": tot[i] / cnt[i], "launches": cnt[i]}
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = 3.5 * tot_fwd_flops / (ms_max * 1e-3) / 1e12
+
+    # fwd / bwd split and hybrid layer mix (dense layers run the same kernels
+    # with the dense-causal layout, make_dense_config)
+    fwd_ms = kernels.get("fwd_sm100", {}).get("avg_ms", float("nan"))
+    bwd_ms = sum(kernels.get(k_, {}).get("avg_ms", 0.0) for k_ in ("bwd_prep", "bwd_dkv_sm100", "bwd_dq_sm100"))
+
+    # roofline of the dominant kernel; algorithmic FLOPs per launch:
+    #   fwd_sm100: F; bwd_dkv: S-recompute + dP + dV + dK = 2F; bwd_dq: dQ = 0.5F
+    alg = {"fwd_sm100": my_fwd_flops, "bwd_dkv_sm100": 2.0 * my_fwd_flops,
+           "bwd_dq_sm100": 0.5 * my_fwd_flops, "bwd_prep": 0.0}
+    dom = max(kernels, key=lambda k_: kernels[k_]["avg_ms"]) if kernels else None
+    pk, pk_kind = peaks()
+    roof = None
+    if dom:
+        ach = alg.get(dom, 0.0) / (kernels[dom]["avg_ms"] * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops"], "traffic": None,
+                "peak_source": f"{pk_kind} bf16_tflops (burst)",
+                "frac_of_sustained": ach / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
+                "alg_flops_per_launch": alg.get(dom, 0.0)}
+
+    line = {
+        "metric": "S2 attn fwd+bwd active-block TFLOP/s @32K", "value": value, "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (U[-1,1] bf16)", "config": config_desc(world),
+        "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+        "dense_equiv_tflops": 3.5 * dense_fwd_total / (ms_max * 1e-3) / 1e12,
+        "dense_causal_fwd_bwd_flops_per_gpu": 3.5 * dense1,
+        "active_fwd_bwd_flops_per_gpu": 3.5 * act1,
+        "kernels": kernels, "roofline": roof, "gpu_launches": int(sum(v_["launches"] for v_ in kernels.values())),
+        "clocks": clk.summary(),
+    }
+
+    # ---- end to end through the public API with host buffers
+    if not args.no_e2e:
+        pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t)  # noqa
+        hq, hk, hv, hdo = pin(q), pin(k), pin(v), pin(do)
+        ho, hl, hdq, hdk, hdv = (torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                                 for t in (out, lse, dq, dk, dv))
+        e2e_steps = max(1, min(args.steps, 5))
+
+        def e2e_step():
+            q.copy_(hq, non_blocking=True)
+            k.copy_(hk, non_blocking=True)
+            v.copy_(hv, non_blocking=True)
+            do.copy_(hdo, non_blocking=True)
+            step()
+            for dst, src in ((ho, out), (hl, lse), (hdq, dq), (hdk, dk), (hdv, dv)):
+                dst.copy_(src, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        e0.record()
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record()
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1) / e2e_steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        ems = float(ems.item())
+        h2d = sum(t.numel() * t.element_size() for t in (q, k, v, do))
+        d2h = sum(t.numel() * t.element_size() for t in (out, lse, dq, dk, dv))
+        line["e2e"] = {"value": 3.5 * tot_fwd_flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
+                       "ms_per_step": ems, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+            val, secs, kind, desc, fl = cpu_sample(heads=(0,))
+            line["cpu_baseline"] = {"value": val, "unit": "TFLOP/s", "cores": host_cores(),
+                                    "kind": kind, "sample": desc, "seconds": secs}
+        except Exception as ex:  # reported, never fatal to the GPU number
+            line["cpu_baseline"] = {"value": None, "error": str(ex)}
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="s2", choices=["s2", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_s2(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -232,6 +232,14 @@ int s2_partition_lpt(int num_units, const int64_t* weights, int num_ranks, int* 
 int s2_plan_fwd_flops(const s2_plan* plan, int batch, int head_dim, double* active_flops,
                       double* dense_causal_flops);
 
+/* ---- per-kernel device timing ------------------------------------------- */
+/* When enabled, every kernel launch records a CUDA event pair on its own
+ * stream.  collect() synchronizes those events, returns per-kernel-name
+ * totals (names: max_kernels x 32 chars) and clears the records. */
+int s2_profile_enable(int enable);
+int s2_profile_collect(int max_kernels, char* names, double* total_ms, int* launches,
+                       int* num_kernels);
+
 #ifdef __cplusplus
 }
 #endif

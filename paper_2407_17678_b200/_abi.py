@@ -106,6 +106,8 @@ SIGNATURES = {
     "s2_partition_lpt": (_I, [_I, _I64P, _I, _IP, _I64P]),
     "s2_plan_fwd_flops": (_I, [_P, _I, _I, ctypes.POINTER(ctypes.c_double),
                                ctypes.POINTER(ctypes.c_double)]),
+    "s2_profile_enable": (_I, [_I]),
+    "s2_profile_collect": (_I, [_I, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), _IP, _IP]),
 }
 
 

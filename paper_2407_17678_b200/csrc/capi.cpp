@@ -584,6 +584,7 @@ int s2_attn_fwd(s2_plan* p, const s2_attn_args* a, s2_stream_t stream) {
             const CUtensorMap mq = s2host::make_map_bf16_3d(a->q, D, N, uint64_t(nu) * hpg, 64, 128);
             const CUtensorMap mk = s2host::make_map_bf16_3d(a->k, D, N, nu, 64, 64);
             const CUtensorMap mv = s2host::make_map_bf16_3d(a->v, D, N, nu, 64, 64);
+            ProfScope prof("fwd_sm100", st);
             e = s2_launch_fwd_sm100(a->head_dim, mq, mk, mv, w->pair.ptr, w->num_pair,
                                     L->d_steps.ptr, static_cast<__nv_bfloat16*>(a->out), a->lse,
                                     a->seq_len, hpg, float(scale * M_LOG2E), num_sms(), st);
@@ -594,6 +595,7 @@ int s2_attn_fwd(s2_plan* p, const s2_attn_args* a, s2_stream_t stream) {
         if (a->head_dim > 256)
             return fail(S2_ERR_UNSUPPORTED, "head_dim > 256 is not supported");
         if ((rc = ensure_csr_uploaded(p))) return rc;
+        ProfScope prof("fwd_simt", st);
         e = s2_launch_fwd_simt(a->dtype == S2_DTYPE_BF16, a->q, a->k, a->v, a->out, a->lse,
                                w->simt_bh.as<int>(), w->simt_head.as<int>(), w->num_bh,
                                p->d_row_ptr.as<int>(), p->d_col_idx.as<int>(),

@@ -7,14 +7,11 @@
 cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* dout,
                                const float* lse, float* delta, float* lse2, int num_bh, int N,
                                int Npad, int D, cudaStream_t stream);
-cudaError_t s2_launch_bwd_sm100(int D, const CUtensorMap& q64, const CUtensorMap& do64,
-                                const CUtensorMap& q128, const CUtensorMap& do128,
-                                const CUtensorMap& k, const CUtensorMap& v, const void* dkv_items,
-                                int num_dkv, const void* dkv_entries, const void* dq_items,
-                                int num_dq, const void* dq_chunks, const float* lse2,
-                                const float* delta, __nv_bfloat16* dq, __nv_bfloat16* dk,
-                                __nv_bfloat16* dv, int N, int Npad, int hpg, float scale,
-                                int num_sms, cudaStream_t stream);
+cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CUtensorMap& dout,
+                                const CUtensorMap& k, const CUtensorMap& v, const void* items,
+                                int num_items, const void* entries, const float* lse2,
+                                const float* delta, __nv_bfloat16* g0, __nv_bfloat16* g1, int N,
+                                int Npad, int hpg, float scale, int num_sms, cudaStream_t stream);
 
 using namespace s2;
 
@@ -68,9 +65,13 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
     const double scale = f.scale != 0.0 ? f.scale : 1.0 / std::sqrt(double(D));
     float* delta = static_cast<float*>(workspace);
     float* lse2 = delta + static_cast<size_t>(nqbh) * Npad;
-    cudaError_t e = s2_launch_bwd_prep(static_cast<const __nv_bfloat16*>(f.out),
-                                       static_cast<const __nv_bfloat16*>(a->dout), f.lse, delta,
-                                       lse2, nqbh, N, Npad, D, st);
+    cudaError_t e;
+    {
+        ProfScope prof("bwd_prep", st);
+        e = s2_launch_bwd_prep(static_cast<const __nv_bfloat16*>(f.out),
+                               static_cast<const __nv_bfloat16*>(a->dout), f.lse, delta, lse2,
+                               nqbh, N, Npad, D, st);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "s2_attn_bwd prep launch");
     try {
         using s2host::make_map_bf16_3d;
@@ -80,12 +81,21 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
         const CUtensorMap do128 = make_map_bf16_3d(a->dout, D, N, nqbh, 64, 128);
         const CUtensorMap mk = make_map_bf16_3d(f.k, D, N, nkv, 64, 64);
         const CUtensorMap mv = make_map_bf16_3d(f.v, D, N, nkv, 64, 64);
-        e = s2_launch_bwd_sm100(D, q64, do64, q128, do128, mk, mv, w->bwd.ptr, w->num_bwd,
-                                L->d_entries.ptr, w->fwd.ptr, w->num_fwd, L->d_chunks.ptr, lse2,
-                                delta, static_cast<__nv_bfloat16*>(a->dq),
-                                static_cast<__nv_bfloat16*>(a->dk),
-                                static_cast<__nv_bfloat16*>(a->dv), N, Npad, hpg, float(scale),
-                                num_sms(), st);
+        {
+            ProfScope prof("bwd_dkv_sm100", st);
+            e = s2_launch_bwd_sm100(0, D, q64, do64, mk, mv, w->bwd.ptr, w->num_bwd,
+                                    L->d_entries.ptr, lse2, delta,
+                                    static_cast<__nv_bfloat16*>(a->dk),
+                                    static_cast<__nv_bfloat16*>(a->dv), N, Npad, hpg,
+                                    float(scale), num_sms(), st);
+        }
+        if (e == cudaSuccess) {
+            ProfScope prof("bwd_dq_sm100", st);
+            e = s2_launch_bwd_sm100(1, D, q128, do128, mk, mv, w->fwd.ptr, w->num_fwd,
+                                    L->d_chunks.ptr, lse2, delta,
+                                    static_cast<__nv_bfloat16*>(a->dq), nullptr, N, Npad, hpg,
+                                    float(scale), num_sms(), st);
+        }
     } catch (const std::exception& ex) {
         return fail(S2_ERR_CUDA, ex.what());
     }

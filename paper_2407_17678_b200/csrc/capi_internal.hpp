@@ -18,4 +18,17 @@ int ensure_csr_uploaded(s2_plan* p);
 Lists* get_lists(s2_plan* p, int seq_len, int* status);
 WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* unit_ids,
                      int* status);
+// RAII: records a CUDA event pair around a launch when profiling is enabled.
+class ProfScope {
+public:
+    ProfScope(const char* name, cudaStream_t st);
+    ~ProfScope();
+
+private:
+    const char* name_;
+    cudaStream_t st_;
+    void* a_ = nullptr;
+    void* b_ = nullptr;
+    bool active_ = false;
+};
 }  // namespace s2

@@ -557,31 +557,22 @@ static cudaError_t launch_bwd(K kern, int smem, int grid, const CUtensorMap& q,
     return cudaGetLastError();
 }
 
-// q64/do64: 64-row boxes (dkv); q128/do128: 128-row boxes (dq); k/v: 64-row boxes.
-cudaError_t s2_launch_bwd_sm100(int D, const CUtensorMap& q64, const CUtensorMap& do64,
-                                const CUtensorMap& q128, const CUtensorMap& do128,
-                                const CUtensorMap& k, const CUtensorMap& v, const void* dkv_items,
-                                int num_dkv, const void* dkv_entries, const void* dq_items,
-                                int num_dq, const void* dq_chunks, const float* lse2,
-                                const float* delta, __nv_bfloat16* dq, __nv_bfloat16* dk,
-                                __nv_bfloat16* dv, int N, int Npad, int hpg, float scale,
-                                int num_sms, cudaStream_t stream) {
+// which = 0: dK/dV kernel (q/do: 64-row boxes); which = 1: dQ kernel (q/do:
+// 128-row boxes).  k/v: 64-row boxes.
+cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CUtensorMap& dout,
+                                const CUtensorMap& k, const CUtensorMap& v, const void* items,
+                                int num_items, const void* entries, const float* lse2,
+                                const float* delta, __nv_bfloat16* g0, __nv_bfloat16* g1, int N,
+                                int Npad, int hpg, float scale, int num_sms, cudaStream_t stream) {
+    if (num_items == 0) return cudaSuccess;
     const float sl2 = scale * 1.4426950408889634f;
-    BwdParams pk{dkv_items, num_dkv, dkv_entries, lse2, delta, dk, dv, N, Npad, hpg, sl2, scale};
-    BwdParams pq{dq_items, num_dq, dq_chunks, lse2, delta, dq, nullptr, N, Npad, hpg, sl2, scale};
-    const int gk = num_dkv < num_sms ? num_dkv : num_sms;
-    const int gq = num_dq < num_sms ? num_dq : num_sms;
-    cudaError_t e = cudaSuccess;
-    if (D == 128) {
-        if (num_dkv) e = launch_bwd(s2_bwd_dkv_kernel<128>, BwdCfg<128>::kDkvSmem, gk, q64, do64, k, v, pk, stream);
-        if (e == cudaSuccess && num_dq)
-            e = launch_bwd(s2_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmem, gq, q128, do128, k, v, pq, stream);
-    } else if (D == 64) {
-        if (num_dkv) e = launch_bwd(s2_bwd_dkv_kernel<64>, BwdCfg<64>::kDkvSmem, gk, q64, do64, k, v, pk, stream);
-        if (e == cudaSuccess && num_dq)
-            e = launch_bwd(s2_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmem, gq, q128, do128, k, v, pq, stream);
-    } else {
-        e = cudaErrorInvalidValue;
-    }
-    return e;
+    BwdParams pp{items, num_items, entries, lse2, delta, g0, g1, N, Npad, hpg, sl2, scale};
+    const int grid = num_items < num_sms ? num_items : num_sms;
+    if (D == 128)
+        return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<128>, BwdCfg<128>::kDkvSmem, grid, q, dout, k, v, pp, stream)
+                          : launch_bwd(s2_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmem, grid, q, dout, k, v, pp, stream);
+    if (D == 64)
+        return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<64>, BwdCfg<64>::kDkvSmem, grid, q, dout, k, v, pp, stream)
+                          : launch_bwd(s2_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmem, grid, q, dout, k, v, pp, stream);
+    return cudaErrorInvalidValue;
 }

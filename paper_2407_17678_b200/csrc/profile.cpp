@@ -1,0 +1,95 @@
+// Per-kernel CUDA-event timing for bench.py (s2_profile_* in s2attn.h).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "capi_internal.hpp"
+
+namespace s2 {
+namespace {
+struct Rec {
+    std::string name;
+    cudaEvent_t a, b;
+};
+std::mutex g_mu;
+bool g_on = false;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t take() {
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+
+ProfScope::ProfScope(const char* name, cudaStream_t st) : name_(name), st_(st) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_on) return;
+    a_ = take();
+    b_ = take();
+    cudaEventRecord(static_cast<cudaEvent_t>(a_), st_);
+    active_ = true;
+}
+
+ProfScope::~ProfScope() {
+    if (!active_) return;
+    cudaEventRecord(static_cast<cudaEvent_t>(b_), st_);
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_recs.push_back({name_, static_cast<cudaEvent_t>(a_), static_cast<cudaEvent_t>(b_)});
+}
+}  // namespace s2
+
+using namespace s2;
+
+extern "C" {
+int s2_profile_enable(int enable) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_on = enable != 0;
+    for (auto& r : g_recs) {
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_recs.clear();
+    return S2_OK;
+}
+
+int s2_profile_collect(int max_kernels, char* names, double* total_ms, int* launches,
+                       int* num_kernels) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    std::map<std::string, std::pair<double, int>> acc;
+    for (auto& r : g_recs) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        auto& x = acc[r.name];
+        x.first += ms;
+        x.second += 1;
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_recs.clear();
+    int n = 0;
+    for (auto& kv : acc) {
+        if (n >= max_kernels) break;
+        if (names) {
+            std::memset(names + 32 * n, 0, 32);
+            std::strncpy(names + 32 * n, kv.first.c_str(), 31);
+        }
+        if (total_ms) total_ms[n] = kv.second.first;
+        if (launches) launches[n] = kv.second.second;
+        ++n;
+    }
+    if (num_kernels) *num_kernels = n;
+    return S2_OK;
+}
+}
