@@ -26,4 +26,20 @@ struct BwdEntry {
     uint32_t mask0, mask1;
 };
 
+// Split-KV decode launch parameters (kernels/decode.cu, capi_decode.cpp).
+struct DecodeParams {
+    const __nv_bfloat16* q;     // [B, H, D]
+    const int64_t* row_ptr;     // [Hkv][NB+1] offsets into slot_idx (rows of the mask)
+    const int* slot_idx;        // slots of each row's key blocks, ascending key block
+    int NB;                     // blocks of the layout
+    int bt;                     // current decode row
+    int last_tokens;            // valid tokens of block bt (the row's last entry)
+    int splits;
+    int blocks_per_split;
+    int H, Hkv, D, hpg;
+    float scale_log2;
+    float* o_part;    // [B, H, splits, D]
+    float* lse_part;  // [B, H, splits] (log2 domain)
+};
+
 }  // namespace s2dev
