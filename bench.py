@@ -347,6 +347,13 @@ def run_s2(args):
         line["e2e"] = {"value": 3.5 * tot_fwd_flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
                        "ms_per_step": ems, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
+    # ---- decode at cfg4 (B=64, 128K context, GQA 32q/8kv, v=8), per GPU
+    if not args.no_decode:
+        try:
+            line["decode"] = bench_decode(args, dev, world)
+        except Exception as ex:  # reported, never fatal to the main number
+            line["decode"] = {"error": str(ex)}
+
     # ---- CPU baseline (rank 0, N=1 only)
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
@@ -364,6 +371,79 @@ def run_s2(args):
         dist.destroy_process_group()
 
 
+def bench_decode(args, dev, world):
+    """cfg4 decode step: 64 sequences x 1 token at position 131071 over the
+    compacted cache; tok/s and achieved HBM GB/s (bytes = retained K/V + q/out)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_17678_b200 as s2
+    from paper_2407_17678_b200 import _abi
+    from paper_2407_17678_b200.decode import KVCache
+
+    Bd, Hq, Hk, T = 64, 32, 8, 131072
+    plan = s2.Plan.from_config(s2.make_s2_config(T, Hq, num_kv_heads=Hk, block_size=64,
+                                                 local_blocks=4, vert_stride=8))
+    cache = KVCache(plan, Bd, D)
+    g = torch.Generator(device=dev).manual_seed(99)
+    kv = torch.empty((Bd, Hk, T, D), device=dev, dtype=torch.bfloat16)
+    kv.normal_(generator=g)
+    cache.prefill(kv, kv)
+    del kv
+    torch.cuda.empty_cache()
+    q = torch.randn((Bd, Hq, D), device=dev, dtype=torch.bfloat16, generator=g)
+    out, lse = cache.decode(q)
+    steps = max(args.steps, 20)
+    for _ in range(max(args.warmup, 3)):
+        cache.decode(q, out=out, lse=lse)
+    torch.cuda.synchronize()
+    lib = _abi.lib()
+    lib.s2_profile_enable(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        cache.decode(q, out=out, lse=lse)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    names = ctypes.create_string_buffer(32 * 16)
+    tot = (ctypes.c_double * 16)()
+    cnt = (ctypes.c_int * 16)()
+    nk = ctypes.c_int()
+    lib.s2_profile_collect(16, names, tot, cnt, ctypes.byref(nk))
+    lib.s2_profile_enable(0)
+    kern = {}
+    for i in range(nk.value):
+        nm = names.raw[32 * i: 32 * i + 32].split(b"\0")[0].decode()
+        kern[nm] = {"avg_ms": tot[i] / cnt[i], "launches": cnt[i]}
+    by = cache.decode_bytes()
+    pool, dense = cache.bytes()
+    pk, pk_kind = peaks()
+    split_ms = kern.get("decode_split", {}).get("avg_ms", ms)
+    ach = by / (split_ms * 1e-3) / 1e9
+    # e2e: q from pinned host, out back to pinned host, every step
+    hq = torch.empty(q.shape, dtype=q.dtype, pin_memory=True).copy_(q)
+    ho = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(steps):
+        q.copy_(hq, non_blocking=True)
+        cache.decode(q, out=out, lse=lse)
+        ho.copy_(out, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1) / steps
+    return {"metric": "decode tok/s (B=64, 128K ctx, 32q/8kv, v=8, compacted cache)",
+            "value": world * Bd / (ms * 1e-3), "unit": "tok/s", "ms_per_step": ms,
+            "kernels": kern, "bytes_per_step": by, "pool_bytes": pool, "dense_cache_bytes": dense,
+            "roofline": {"kernel": "decode_split", "bound": "hbm", "achieved": ach,
+                         "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
+                         "frac_of_8TBps": ach / 8000.0, "traffic": None,
+                         "peak_source": f"{pk_kind} hbm_gbs"},
+            "e2e": {"value": world * Bd / (ems * 1e-3), "unit": "tok/s", "ms_per_step": ems,
+                    "h2d_bytes_per_step": q.numel() * 2, "d2h_bytes_per_step": out.numel() * 2}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -372,6 +452,7 @@ def main():
     ap.add_argument("--impl", default="s2", choices=["s2", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -94,11 +94,14 @@ class HeadParallelPlan:
 
 
 def head_parallel_forward(plan, q, k, v, rank: int, world_size: int, *, group=None,
-                          scale: Optional[float] = None, hp: Optional[HeadParallelPlan] = None):
+                          scale: Optional[float] = None, hp: Optional[HeadParallelPlan] = None,
+                          local_fn=None):
     """Shard units over ranks, run the local sparse forward, all-gather O and lse.
 
     q [B,H,N,D], k/v [B,Hkv,N,D] are the full tensors (each rank reads only its
-    units).  Returns full (out [B,H,N,D], lse [B,H,N])."""
+    units).  Returns full (out [B,H,N,D], lse [B,H,N]).  local_fn(plan, q_units,
+    k_units, v_units, unit_ids) -> (out_units, lse_units) defaults to the sm_100a
+    kernel (s2_attn_fwd)."""
     from .attention import s2_attn_fwd
 
     B, H, N, D = q.shape
@@ -108,7 +111,10 @@ def head_parallel_forward(plan, q, k, v, rank: int, world_size: int, *, group=No
         ql = hp.scatter_q(q, rank)
         kl = hp.scatter_kv(k, rank)
         vl = hp.scatter_kv(v, rank)
-        out_l, lse_l = s2_attn_fwd(plan, ql, kl, vl, scale=scale, unit_ids=units)
+        if local_fn is None:
+            out_l, lse_l = s2_attn_fwd(plan, ql, kl, vl, scale=scale, unit_ids=units)
+        else:
+            out_l, lse_l = local_fn(plan, ql, kl, vl, units)
     else:
         import torch
 

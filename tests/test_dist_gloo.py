@@ -1,0 +1,102 @@
+"""Head-parallel multi-GPU path on CPU: world_size 2 over gloo.
+
+Exercises the partitioner, unit scatter, the single all-gather and the
+unpack of HeadParallelPlan exactly as bench.py / head_parallel_forward use
+them, with the oracle standing in for the local kernel (test-only).  The
+gathered output must be bit-identical to a single-process run
+(head-permutation exactness, test_attention.cpp:217-240).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from helpers import single
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_local(cfg):
+    import torch
+
+    import oracle
+
+    B = cfg.num_blocks()
+    rp_all, ci_all = oracle.csr_all(cfg)
+    H, Hkv = cfg.num_heads, cfg.kv_heads()
+    hpg = H // Hkv
+    offs = np.concatenate([[0], np.cumsum([rp_all[h * (B + 1) + B] for h in range(H)])])
+
+    def fn(plan, ql, kl, vl, units):
+        U, _, N, D = ql.shape
+        outs, lses = [], []
+        for i, u in enumerate(units):
+            g = int(u) % Hkv
+            heads = list(range(g * hpg, (g + 1) * hpg))
+            rp = np.concatenate([rp_all[h * (B + 1):(h + 1) * (B + 1)] for h in heads])
+            ci = np.concatenate([ci_all[offs[h]:offs[h + 1]] for h in heads])
+            o, l = oracle.attn_fwd(ql[i].numpy().ravel(), kl[i].numpy().ravel(),
+                                   vl[i].numpy().ravel(), rp, ci, 1, hpg, 1, N, D,
+                                   cfg.block_size)
+            outs.append(torch.from_numpy(o).reshape(1, hpg, N, D))
+            lses.append(torch.from_numpy(l.astype(np.float32)).reshape(1, hpg, N))
+        return torch.cat(outs), torch.cat(lses)
+
+    return fn
+
+
+def _worker(rank, world, port, cfg, batch, D, res_path):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_17678_b200 as s2
+    from paper_2407_17678_b200.dist import HeadParallelPlan, head_parallel_forward
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plan = s2.Plan.from_config(cfg)
+    N, H, Hkv = cfg.seq_len, cfg.num_heads, cfg.kv_heads()
+    g = torch.Generator().manual_seed(5)
+    q = torch.rand((batch, H, N, D), generator=g) * 2 - 1
+    k = torch.rand((batch, Hkv, N, D), generator=g) * 2 - 1
+    v = torch.rand((batch, Hkv, N, D), generator=g) * 2 - 1
+    hp = HeadParallelPlan(plan, batch, world)
+    out, lse = head_parallel_forward(plan, q, k, v, rank, world, hp=hp,
+                                     local_fn=_oracle_local(cfg))
+    if rank == 0:
+        np.savez(res_path, out=out.numpy(), lse=lse.numpy(), q=q.numpy(), k=k.numpy(),
+                 v=v.numpy(), load=hp.load, owner=hp.owner)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", [
+    (single(512, 64, 4, 2, 3), 2, 16),          # MHA, batch 2
+    (single(640, 64, 8, 2, 4, kv=2), 3, 8),     # GQA 4:1, batch 3 (uneven units)
+])
+def test_head_parallel_world2_gloo_matches_single_process(case, tmp_path):
+    import torch.multiprocessing as mp
+
+    import oracle
+
+    cfg, batch, D = case
+    res = str(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(2, _free_port(), cfg, batch, D, res), nprocs=2, join=True)
+    r = np.load(res)
+    H, Hkv, N = cfg.num_heads, cfg.kv_heads(), cfg.seq_len
+    rp, ci = oracle.csr_all(cfg)
+    ro, rl = oracle.attn_fwd(r["q"].ravel(), r["k"].ravel(), r["v"].ravel(), rp, ci, batch, H,
+                             Hkv, N, D, cfg.block_size)
+    np.testing.assert_array_equal(r["out"].ravel(), ro)
+    np.testing.assert_array_equal(r["lse"].ravel(), rl.astype(np.float32))
+    # both ranks got work and LPT balanced it
+    assert set(r["owner"].tolist()) == {0, 1}
+    assert r["load"].max() <= r["load"].sum() / 2 * 1.5
