@@ -232,6 +232,14 @@ int s2_partition_lpt(int num_units, const int64_t* weights, int num_ranks, int* 
 int s2_plan_fwd_flops(const s2_plan* plan, int batch, int head_dim, double* active_flops,
                       double* dense_causal_flops);
 
+/* ---- device memory helpers (so FFI callers need no CUDA runtime) --------- */
+int s2_device_count(int* count);
+int s2_device_malloc(void** ptr, size_t bytes);
+int s2_device_free(void* ptr);
+int s2_memcpy_h2d(void* dst, const void* src, size_t bytes, s2_stream_t stream);
+int s2_memcpy_d2h(void* dst, const void* src, size_t bytes, s2_stream_t stream);
+int s2_stream_synchronize(s2_stream_t stream);
+
 /* ---- per-kernel device timing ------------------------------------------- */
 /* When enabled, every kernel launch records a CUDA event pair on its own
  * stream.  collect() synchronizes those events, returns per-kernel-name

@@ -1,0 +1,58 @@
+// Drop-in replacement header for /root/reference/proj/include/shardattn/attention.hpp
+// (attention.hpp:17-66).  Host tensors in and out exactly as the reference;
+// the work runs on the B200 behind include/s2attn.h:
+//   streaming_sharded_attention / dsplit_attention -> fp32 sm_100a kernel
+//   naive_masked_attention / dense_masked_attention -> the same kernel after
+//     the reference's mask validation (dense: finiteness + causal masks)
+// Extensions in the house style (the reference has neither):
+//   streaming_sharded_attention_backward -> tcgen05 bf16 backward kernels
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "shardattn/csr.hpp"
+#include "shardattn/pattern.hpp"
+
+namespace shardattn {
+
+struct AttentionTensors {
+    int num_heads = 0;
+    int seq_len = 0;
+    int head_dim = 0;
+    double scale = 0.0;
+
+    std::vector<float> q, k, v;
+    std::vector<float> out;
+    std::vector<double> lse;
+
+    static AttentionTensors zeros(int num_heads, int seq_len, int head_dim);
+    static AttentionTensors random(int num_heads, int seq_len, int head_dim, std::uint64_t seed);
+
+    std::size_t idx(int head, int token, int component) const {
+        return (static_cast<std::size_t>(head) * seq_len + token) * head_dim + component;
+    }
+    std::size_t row_index(int head, int token) const {
+        return static_cast<std::size_t>(head) * seq_len + token;
+    }
+};
+
+void naive_masked_attention(AttentionTensors& t, const std::vector<HeadBlockMask>& masks,
+                            int block_size);
+void dense_masked_attention(AttentionTensors& t, const std::vector<HeadBlockMask>& masks,
+                            int block_size);
+void streaming_sharded_attention(AttentionTensors& t, const std::vector<CsrMask>& csr,
+                                 int block_size);
+void dsplit_attention(AttentionTensors& t, const std::vector<CsrMask>& csr, int block_size,
+                      int num_splits);
+
+/// Gradients of sum(dout * out) w.r.t. q, k, v for the forward above (inputs
+/// rounded to bf16, tensor-core kernels; tolerance 1e-2).  Shapes as q/k/v.
+struct AttentionGrads {
+    std::vector<float> dq, dk, dv;
+};
+void streaming_sharded_attention_backward(const AttentionTensors& t,
+                                          const std::vector<CsrMask>& csr, int block_size,
+                                          const std::vector<float>& dout, AttentionGrads& grads);
+
+}  // namespace shardattn

@@ -106,6 +106,12 @@ SIGNATURES = {
     "s2_partition_lpt": (_I, [_I, _I64P, _I, _IP, _I64P]),
     "s2_plan_fwd_flops": (_I, [_P, _I, _I, ctypes.POINTER(ctypes.c_double),
                                ctypes.POINTER(ctypes.c_double)]),
+    "s2_device_count": (_I, [_IP]),
+    "s2_device_malloc": (_I, [ctypes.POINTER(_P), ctypes.c_size_t]),
+    "s2_device_free": (_I, [_P]),
+    "s2_memcpy_h2d": (_I, [_P, _P, ctypes.c_size_t, _P]),
+    "s2_memcpy_d2h": (_I, [_P, _P, ctypes.c_size_t, _P]),
+    "s2_stream_synchronize": (_I, [_P]),
     "s2_profile_enable": (_I, [_I]),
     "s2_profile_collect": (_I, [_I, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), _IP, _IP]),
 }

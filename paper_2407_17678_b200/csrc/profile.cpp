@@ -93,3 +93,39 @@ int s2_profile_collect(int max_kernels, char* names, double* total_ms, int* laun
     return S2_OK;
 }
 }
+
+extern "C" {
+int s2_device_count(int* count) {
+    if (!count) return fail(S2_ERR_INVALID_ARGUMENT, "null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+    *count = n;
+    return S2_OK;
+}
+int s2_device_malloc(void** ptr, size_t bytes) {
+    if (!ptr) return fail(S2_ERR_INVALID_ARGUMENT, "null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        return fail(S2_ERR_NO_DEVICE, "no CUDA device: the S2 kernels need a B200");
+    cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 16);
+    return e == cudaSuccess ? S2_OK : cuda_fail(e, "cudaMalloc");
+}
+int s2_device_free(void* ptr) {
+    cudaError_t e = cudaFree(ptr);
+    return e == cudaSuccess ? S2_OK : cuda_fail(e, "cudaFree");
+}
+int s2_memcpy_h2d(void* dst, const void* src, size_t bytes, s2_stream_t stream) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice,
+                                    reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? S2_OK : cuda_fail(e, "cudaMemcpyAsync H2D");
+}
+int s2_memcpy_d2h(void* dst, const void* src, size_t bytes, s2_stream_t stream) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost,
+                                    reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? S2_OK : cuda_fail(e, "cudaMemcpyAsync D2H");
+}
+int s2_stream_synchronize(s2_stream_t stream) {
+    cudaError_t e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? S2_OK : cuda_fail(e, "cudaStreamSynchronize");
+}
+}
