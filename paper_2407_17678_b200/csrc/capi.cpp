@@ -12,9 +12,9 @@
 #include "tma_host.hpp"
 
 cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtensorMap& k,
-                                const CUtensorMap& v, const void* items, int num_items,
-                                const void* steps, __nv_bfloat16* out, float* lse, int seq_len,
-                                int hpg, float scale_log2, int num_sms, cudaStream_t stream);
+                                const CUtensorMap& v, const void* items, const int* sched,
+                                int grid, const void* steps, __nv_bfloat16* out, float* lse,
+                                int seq_len, int hpg, float scale_log2, cudaStream_t stream);
 cudaError_t s2_launch_fwd_simt(bool bf16, const void* q, const void* k, const void* v, void* out,
                                float* lse, const int* bh_list, const int* head_of, int num_bh,
                                const int* row_ptr, const int* col_idx, const int64_t* col_off,
@@ -119,6 +119,39 @@ Lists* get_lists(s2_plan* p, int seq_len, int* status) {
     return L;
 }
 
+// Static persistent-CTA schedule: items are visited in `order` (head-major,
+// heaviest first inside a head) and each goes to the CTA whose queue
+// finishes earliest (greedy list scheduling).  CTAs therefore sweep the
+// heads together — a head's K/V (or Q/dO) stays L2-resident while every CTA
+// works on it — and the tail is made of the lightest items.  Returns the
+// items regrouped per CTA plus offsets [grid + 1].
+template <class T, class Cost, class Key>
+static std::vector<int32_t> schedule_items(std::vector<T>& items, int grid, Cost cost, Key key) {
+    std::stable_sort(items.begin(), items.end(), [&](const T& a, const T& b) {
+        const auto ka = key(a), kb = key(b);
+        if (ka != kb) return ka < kb;
+        return cost(a) > cost(b);
+    });
+    std::vector<std::vector<T>> per(grid);
+    std::vector<std::pair<int64_t, int>> heap;  // (finish time, cta) min-heap
+    for (int c = 0; c < grid; ++c) heap.push_back({0, c});
+    std::make_heap(heap.begin(), heap.end(), std::greater<>());
+    for (const T& it : items) {
+        std::pop_heap(heap.begin(), heap.end(), std::greater<>());
+        auto& top = heap.back();
+        per[top.second].push_back(it);
+        top.first += cost(it) + 4;  // + fixed per-item overhead
+        std::push_heap(heap.begin(), heap.end(), std::greater<>());
+    }
+    std::vector<int32_t> off(grid + 1, 0);
+    items.clear();
+    for (int c = 0; c < grid; ++c) {
+        items.insert(items.end(), per[c].begin(), per[c].end());
+        off[c + 1] = static_cast<int32_t>(items.size());
+    }
+    return off;
+}
+
 // Units are (batch, kv-group); local data index of query head j of the
 // ui-th listed unit is ui*hpg + j (= b*H + h when every unit is listed).
 WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* unit_ids,
@@ -166,9 +199,10 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
                 const int cnt = static_cast<int>(L->fwd.offset[w_ + 1] - off);
                 fi.push_back({bh[i], head[i], t, cnt, off});
             }
-        std::stable_sort(fi.begin(), fi.end(), [](const s2dev::FwdItem& a, const s2dev::FwdItem& b) {
-            return a.chunk_cnt > b.chunk_cnt;
-        });
+        const int grid = num_sms();
+        const std::vector<int32_t> off_fwd = schedule_items(
+            fi, grid, [](const s2dev::FwdItem& a) { return int64_t(a.chunk_cnt); },
+            [](const s2dev::FwdItem& a) { return a.bh; });
         struct PairItem {
             int32_t bh, qpair, nsteps, has_b;
             int64_t step_off;
@@ -182,11 +216,13 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
                 pi.push_back({bh[i], q, static_cast<int32_t>(L->pairs.offset[w_ + 1] - off),
                               2 * q + 1 < nt ? 1 : 0, off});
             }
-        std::stable_sort(pi.begin(), pi.end(), [](const PairItem& a, const PairItem& b) {
-            return a.nsteps * (1 + a.has_b) > b.nsteps * (1 + b.has_b);
-        });
+        const std::vector<int32_t> off_pair = schedule_items(
+            pi, grid, [](const PairItem& a) { return int64_t(a.nsteps) * (1 + a.has_b); },
+            [](const PairItem& a) { return a.bh; });
         w->num_pair = static_cast<int>(pi.size());
-        if ((e = upload(w->pair, pi.data(), pi.size() * sizeof(PairItem))) != cudaSuccess) {
+        if ((e = upload(w->pair, pi.data(), pi.size() * sizeof(PairItem))) != cudaSuccess ||
+            (e = upload(w->pair_sched, off_pair.data(), off_pair.size() * sizeof(int32_t))) != cudaSuccess ||
+            (e = upload(w->fwd_sched, off_fwd.data(), off_fwd.size() * sizeof(int32_t))) != cudaSuccess) {
             *status = cuda_fail(e, "uploading work items");
             return nullptr;
         }
@@ -196,13 +232,15 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
             for (const BwdTile& t : L->bwd.tiles)
                 if (t.group == g) bi.push_back({static_cast<int>(ui), t.c0, t.c1, t.count, t.offset});
         }
-        std::stable_sort(bi.begin(), bi.end(), [](const s2dev::BwdItem& a, const s2dev::BwdItem& b) {
-            return a.count > b.count;
-        });
+        const std::vector<int32_t> off_bwd = schedule_items(
+            bi, grid, [hpg](const s2dev::BwdItem& a) { return int64_t(a.count) * hpg; },
+            [](const s2dev::BwdItem& a) { return a.kvbh; });
         w->num_fwd = static_cast<int>(fi.size());
         w->num_bwd = static_cast<int>(bi.size());
+        w->grid = grid;
         if ((e = upload(w->fwd, fi.data(), fi.size() * sizeof(s2dev::FwdItem))) != cudaSuccess ||
-            (e = upload(w->bwd, bi.data(), bi.size() * sizeof(s2dev::BwdItem))) != cudaSuccess) {
+            (e = upload(w->bwd, bi.data(), bi.size() * sizeof(s2dev::BwdItem))) != cudaSuccess ||
+            (e = upload(w->bwd_sched, off_bwd.data(), off_bwd.size() * sizeof(int32_t))) != cudaSuccess) {
             *status = cuda_fail(e, "uploading work items");
             return nullptr;
         }
@@ -585,9 +623,9 @@ int s2_attn_fwd(s2_plan* p, const s2_attn_args* a, s2_stream_t stream) {
             const CUtensorMap mk = s2host::make_map_bf16_3d(a->k, D, N, nu, 64, 64);
             const CUtensorMap mv = s2host::make_map_bf16_3d(a->v, D, N, nu, 64, 64);
             ProfScope prof("fwd_sm100", st);
-            e = s2_launch_fwd_sm100(a->head_dim, mq, mk, mv, w->pair.ptr, w->num_pair,
-                                    L->d_steps.ptr, static_cast<__nv_bfloat16*>(a->out), a->lse,
-                                    a->seq_len, hpg, float(scale * M_LOG2E), num_sms(), st);
+            e = s2_launch_fwd_sm100(a->head_dim, mq, mk, mv, w->pair.ptr, w->pair_sched.as<int>(),
+                                    w->grid, L->d_steps.ptr, static_cast<__nv_bfloat16*>(a->out),
+                                    a->lse, a->seq_len, hpg, float(scale * M_LOG2E), st);
         } catch (const std::exception& ex) {
             return fail(S2_ERR_CUDA, ex.what());
         }

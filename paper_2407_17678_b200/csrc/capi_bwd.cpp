@@ -9,9 +9,10 @@ cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* do
                                int Npad, int D, cudaStream_t stream);
 cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CUtensorMap& dout,
                                 const CUtensorMap& k, const CUtensorMap& v, const void* items,
-                                int num_items, const void* entries, const float* lse2,
-                                const float* delta, __nv_bfloat16* g0, __nv_bfloat16* g1, int N,
-                                int Npad, int hpg, float scale, int num_sms, cudaStream_t stream);
+                                const int* sched, int grid, const void* entries,
+                                const float* lse2, const float* delta, __nv_bfloat16* g0,
+                                __nv_bfloat16* g1, int N, int Npad, int hpg, float scale,
+                                cudaStream_t stream);
 
 using namespace s2;
 
@@ -83,18 +84,18 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
         const CUtensorMap mv = make_map_bf16_3d(f.v, D, N, nkv, 64, 64);
         {
             ProfScope prof("bwd_dkv_sm100", st);
-            e = s2_launch_bwd_sm100(0, D, q64, do64, mk, mv, w->bwd.ptr, w->num_bwd,
-                                    L->d_entries.ptr, lse2, delta,
+            e = s2_launch_bwd_sm100(0, D, q64, do64, mk, mv, w->bwd.ptr, w->bwd_sched.as<int>(),
+                                    w->grid, L->d_entries.ptr, lse2, delta,
                                     static_cast<__nv_bfloat16*>(a->dk),
                                     static_cast<__nv_bfloat16*>(a->dv), N, Npad, hpg,
-                                    float(scale), num_sms(), st);
+                                    float(scale), st);
         }
         if (e == cudaSuccess) {
             ProfScope prof("bwd_dq_sm100", st);
-            e = s2_launch_bwd_sm100(1, D, q128, do128, mk, mv, w->fwd.ptr, w->num_fwd,
-                                    L->d_chunks.ptr, lse2, delta,
+            e = s2_launch_bwd_sm100(1, D, q128, do128, mk, mv, w->fwd.ptr, w->fwd_sched.as<int>(),
+                                    w->grid, L->d_chunks.ptr, lse2, delta,
                                     static_cast<__nv_bfloat16*>(a->dq), nullptr, N, Npad, hpg,
-                                    float(scale), num_sms(), st);
+                                    float(scale), st);
         }
     } catch (const std::exception& ex) {
         return fail(S2_ERR_CUDA, ex.what());

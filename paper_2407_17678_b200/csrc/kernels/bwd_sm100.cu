@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) s2_bwd_prep_kernel(const __nv_bfloat16* _
 
 struct BwdParams {
     const void* items;
-    int num_items;
+    const int* sched;     // [grid + 1] item range of each CTA (host-side schedule)
     const void* entries;  // BwdEntry (dkv) or int2 chunks (dq)
     const float* lse2;    // [num_qbh][Npad], log2 domain, +inf padding
     const float* delta;   // [num_qbh][Npad]
@@ -67,7 +67,15 @@ struct BwdParams {
     __nv_bfloat16* g1;    // dkv: dV
     int N, Npad, hpg;
     float scale_log2, scale;
+    long long* trace;  // debug: per-step clock64 of CTA 0 (nullptr = off)
+    int debug;         // debug ablations (0 in production)
 };
+
+#define S2TRACE(slot, n)                                                       \
+    do {                                                                       \
+        if (p.trace && blockIdx.x == 0 && (n) < 2048)                          \
+            p.trace[(slot) * 2048 + (n)] = clock64();                          \
+    } while (0)
 
 template <int D>
 struct BwdCfg {
@@ -76,7 +84,8 @@ struct BwdCfg {
     static constexpr int kTile64 = kSub * 8192;    // 64 rows x D bf16
     static constexpr int kNST = 4;
     // dkv: resident K, V (128 keys); stages: Q64, dO64, lse2[64], delta[64]
-    static constexpr int kDkvStage = 2 * kTile64 + 512;
+    // lse/delta (512 B) padded so every stage stays 1024-B aligned (SW128 atoms).
+    static constexpr int kDkvStage = 2 * kTile64 + 1024;
     static constexpr int kDkvSmem = 1024 + 2 * kTile128 + kNST * kDkvStage;
     // dq: resident Q, dO (128 rows); stages: K64, V64
     static constexpr int kDqStage = 2 * kTile64;
@@ -141,7 +150,7 @@ __global__ void __launch_bounds__(384, 1)
             tma_prefetch(&tmK);
             tma_prefetch(&tmV);
             uint32_t it_cnt = 0, st_it = 0;
-            for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+            for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
                 const BwdItem it = items[i];
                 if (it_cnt > 0) mbar_wait(smem_u32(&bar_kve), (it_cnt - 1) & 1);
                 const int nc = it.c1 >= 0 ? 2 : 1;
@@ -181,21 +190,22 @@ __global__ void __launch_bounds__(384, 1)
             constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);
             constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
             uint32_t it_cnt = 0, st_it = 0, n_glob = 0;
-            for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+            for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
                 const BwdItem it = items[i];
                 mbar_wait(smem_u32(&bar_kvf), it_cnt & 1);
-                tc_fence_after();
                 bool first = true;
                 int prev_st = -1;
                 uint32_t prev_n = 0;
                 auto accumulate = [&](uint32_t n, int st) {
                     const int b = n & 1;
+                    S2TRACE(3, n);
                     mbar_wait(smem_u32(&bar_p[b]), (n >> 1) & 1);
+                    S2TRACE(4, n);
                     if (first && it_cnt > 0) mbar_wait(smem_u32(&bar_ae), (it_cnt - 1) & 1);
-                    tc_fence_after();
+                    tc_fence_after();  // A operands (P^T, dS^T) were written to TMEM by tcgen05.st
                     const uint32_t base = sSt + st * C::kDkvStage;
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
+                    for (int kk = 0; kk < ((p.debug & 2) ? 0 : 4); ++kk) {
                         const uint32_t acc = (first && kk == 0) ? 0u : 1u;
                         // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
                         mma_ts(tmem + 256, tmem + b * 64 + kk * 8,
@@ -212,8 +222,9 @@ __global__ void __launch_bounds__(384, 1)
                         for (int half = 0; half < 2; ++half) {
                             if (!half_active(en, half)) continue;
                             const int st = st_it % NST;
+                            S2TRACE(0, n_glob);
                             mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
-                            tc_fence_after();
+                            S2TRACE(1, n_glob);
                             const uint32_t base = sSt + st * C::kDkvStage;
                             const int b = n_glob & 1;
 #pragma unroll
@@ -228,6 +239,7 @@ __global__ void __launch_bounds__(384, 1)
                                        idS, kk > 0);
                             }
                             mma_commit(smem_u32(&bar_s[b]));
+                            S2TRACE(2, n_glob);
                             if (prev_st >= 0) accumulate(prev_n, prev_st);
                             prev_st = st;
                             prev_n = n_glob;
@@ -248,7 +260,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const float sl2 = p.scale_log2;
         uint32_t it_cnt = 0, st_it = 0, n_glob = 0;
-        for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+        for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
             const BwdItem it = items[i];
             const int hk = kr >> 6;
             const int chunk = hk ? it.c1 : it.c0;
@@ -262,40 +274,71 @@ __global__ void __launch_bounds__(384, 1)
                         if (!half_active(en, half)) continue;
                         const int st = st_it % NST;
                         const int b = n_glob & 1;
+                        if (tid == 128) S2TRACE(5, n_glob);
                         mbar_wait(smem_u32(&bar_s[b]), (n_glob >> 1) & 1);
+                        if (tid == 128) S2TRACE(6, n_glob);
                         tc_fence_after();
+                        if (p.debug & 1) {
+                            tc_fence_before();
+                            mbar_arrive(smem_u32(&bar_p[b]));
+                            ++n_glob;
+                            ++st_it;
+                            continue;
+                        }
                         uint32_t su[32], du[32];
                         tmem_ld32(tmem + b * 64 + wg * 32 + lane_off, su);
                         tmem_ld32(tmem + 128 + b * 64 + wg * 32 + lane_off, du);
                         const uint32_t m = key_ok ? (hk ? en.mask1 : en.mask0) : 0u;
-                        const float* sl = reinterpret_cast<const float*>(smem + (sSt - sK) + st * C::kDkvStage + 2 * C::kTile64);
+                        // lse2 / delta of my 32 q columns: shared-space vector loads (broadcast).
+                        // They were written by a bulk copy: observe its barrier ourselves
+                        // (already complete; the stage cannot be refilled before our P).
+                        mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
+                        const uint32_t sl = sSt + st * C::kDkvStage + 2 * C::kTile64 + wg * 128;
                         const int g0 = half * 4 + wg * 2;  // q row groups of my 32 columns
                         const bool on0 = (m >> (g0 * 4 + cg)) & 1u;
                         const bool on1 = (m >> ((g0 + 1) * 4 + cg)) & 1u;
                         const int q0 = en.qtile * 128 + half * 64 + wg * 32;
+                        float l2v[32], dlv[32];
+#pragma unroll
+                        for (int c = 0; c < 32; c += 4) {
+                            const float4 a = lds_f4(sl + c * 4), d4 = lds_f4(sl + 256 + c * 4);
+                            l2v[c] = a.x; l2v[c + 1] = a.y; l2v[c + 2] = a.z; l2v[c + 3] = a.w;
+                            dlv[c] = d4.x; dlv[c + 1] = d4.y; dlv[c + 2] = d4.z; dlv[c + 3] = d4.w;
+                        }
                         tmem_ld_wait();
                         uint32_t pk[16], dk[16];
+                        if (on0 && on1 && key_pos <= q0) {
+                            // fully attended 32 columns, no causal cut: no per-element masking
 #pragma unroll
-                        for (int c = 0; c < 32; c += 2) {
-                            float pv[2], dv[2];
-#pragma unroll
-                            for (int u = 0; u < 2; ++u) {
-                                const int cc = c + u;
-                                const bool ok = (cc < 16 ? on0 : on1) && key_pos <= q0 + cc;
-                                const float l2 = sl[wg * 32 + cc];
-                                const float dl = sl[64 + wg * 32 + cc];
-                                const float pe = fast_exp2(fmaf(__uint_as_float(su[cc]), sl2, -l2));
-                                pv[u] = ok ? pe : 0.f;
-                                dv[u] = ok ? pe * (__uint_as_float(du[cc]) - dl) : 0.f;
+                            for (int c = 0; c < 32; c += 2) {
+                                const float p0 = fast_exp2(fmaf(__uint_as_float(su[c]), sl2, -l2v[c]));
+                                const float p1 = fast_exp2(fmaf(__uint_as_float(su[c + 1]), sl2, -l2v[c + 1]));
+                                pk[c >> 1] = pack_bf16(p0, p1);
+                                dk[c >> 1] = pack_bf16(p0 * (__uint_as_float(du[c]) - dlv[c]),
+                                                       p1 * (__uint_as_float(du[c + 1]) - dlv[c + 1]));
                             }
-                            pk[c >> 1] = pack_bf16(pv[0], pv[1]);
-                            dk[c >> 1] = pack_bf16(dv[0], dv[1]);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 32; c += 2) {
+                                float pv[2], dv[2];
+#pragma unroll
+                                for (int u = 0; u < 2; ++u) {
+                                    const int cc = c + u;
+                                    const bool ok = (cc < 16 ? on0 : on1) && key_pos <= q0 + cc;
+                                    const float pe = fast_exp2(fmaf(__uint_as_float(su[cc]), sl2, -l2v[cc]));
+                                    pv[u] = ok ? pe : 0.f;
+                                    dv[u] = ok ? pe * (__uint_as_float(du[cc]) - dlv[cc]) : 0.f;
+                                }
+                                pk[c >> 1] = pack_bf16(pv[0], pv[1]);
+                                dk[c >> 1] = pack_bf16(dv[0], dv[1]);
+                            }
                         }
                         tmem_st16(tmem + b * 64 + wg * 16 + lane_off, pk);
                         tmem_st16(tmem + 128 + b * 64 + wg * 16 + lane_off, dk);
                         tmem_st_wait();
                         tc_fence_before();
                         mbar_arrive(smem_u32(&bar_p[b]));
+                        if (tid == 128) S2TRACE(7, n_glob);
                         ++n_glob;
                         ++st_it;
                     }
@@ -385,7 +428,7 @@ __global__ void __launch_bounds__(384, 1)
             tma_prefetch(&tmV);
             const uint64_t keep = policy_evict_last();
             uint32_t it_cnt = 0, st_it = 0;
-            for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+            for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
                 const FwdItem it = items[i];
                 const int kvbh = it.bh / p.hpg;
                 if (it_cnt > 0) mbar_wait(smem_u32(&bar_qe), (it_cnt - 1) & 1);
@@ -411,16 +454,15 @@ __global__ void __launch_bounds__(384, 1)
             constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);
             constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
             uint32_t it_cnt = 0, st_it = 0, n_glob = 0;
-            for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+            for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
                 const FwdItem it = items[i];
                 mbar_wait(smem_u32(&bar_qf), it_cnt & 1);
-                tc_fence_after();
                 bool first = true;
                 auto accumulate = [&](uint32_t n, int st) {
                     const int b = n & 1;
                     mbar_wait(smem_u32(&bar_p[b]), (n >> 1) & 1);
                     if (first && it_cnt > 0) mbar_wait(smem_u32(&bar_ae), (it_cnt - 1) & 1);
-                    tc_fence_after();
+                    tc_fence_after();  // A operand (dS) was written to TMEM by tcgen05.st
                     const uint32_t base = sSt + st * C::kDqStage;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)  // dQ += dS K  (K chunk as MN-major B)
@@ -435,7 +477,6 @@ __global__ void __launch_bounds__(384, 1)
                 for (int n = 0; n < it.chunk_cnt; ++n, ++st_it, ++n_glob) {
                     const int st = st_it % NST;
                     mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
-                    tc_fence_after();
                     const uint32_t base = sSt + st * C::kDqStage;
                     const int b = n_glob & 1;
 #pragma unroll
@@ -464,7 +505,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const float sl2 = p.scale_log2;
         uint32_t it_cnt = 0, n_glob = 0;
-        for (int i = blockIdx.x; i < p.num_items; i += gridDim.x, ++it_cnt) {
+        for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
             const FwdItem it = items[i];
             const int q_pos = it.qtile * 128 + r;
             const size_t lrow = static_cast<size_t>(it.bh) * p.Npad + q_pos;
@@ -484,17 +525,27 @@ __global__ void __launch_bounds__(384, 1)
                 const int k0 = ch.x * 64 + wg * 32;
                 tmem_ld_wait();
                 uint32_t dk[16];
+                if (on0 && on1 && k0 + 31 <= q_pos) {
 #pragma unroll
-                for (int c = 0; c < 32; c += 2) {
-                    float dv[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int cc = c + u;
-                        const bool ok = (cc < 16 ? on0 : on1) && k0 + cc <= q_pos;
-                        const float pe = fast_exp2(fmaf(__uint_as_float(su[cc]), sl2, -l2));
-                        dv[u] = ok ? pe * (__uint_as_float(du[cc]) - dl) : 0.f;
+                    for (int c = 0; c < 32; c += 2) {
+                        const float p0 = fast_exp2(fmaf(__uint_as_float(su[c]), sl2, -l2));
+                        const float p1 = fast_exp2(fmaf(__uint_as_float(su[c + 1]), sl2, -l2));
+                        dk[c >> 1] = pack_bf16(p0 * (__uint_as_float(du[c]) - dl),
+                                               p1 * (__uint_as_float(du[c + 1]) - dl));
                     }
-                    dk[c >> 1] = pack_bf16(dv[0], dv[1]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        float dv[2];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int cc = c + u;
+                            const bool ok = (cc < 16 ? on0 : on1) && k0 + cc <= q_pos;
+                            const float pe = fast_exp2(fmaf(__uint_as_float(su[cc]), sl2, -l2));
+                            dv[u] = ok ? pe * (__uint_as_float(du[cc]) - dl) : 0.f;
+                        }
+                        dk[c >> 1] = pack_bf16(dv[0], dv[1]);
+                    }
                 }
                 tmem_st16(tmem + 128 + b * 64 + wg * 16 + lane_off, dk);
                 tmem_st_wait();
@@ -538,6 +589,12 @@ __global__ void __launch_bounds__(384, 1)
 
 using namespace s2dev;
 
+static long long* g_trace = nullptr;
+static int g_debug = 0;
+extern "C" void s2_debug_set_mode(int m) { g_debug = m; }
+// Debug hook (not in s2attn.h): a device buffer of 8 x 2048 int64 for CTA-0 step timestamps.
+extern "C" void s2_debug_set_trace(void* dev_buf) { g_trace = static_cast<long long*>(dev_buf); }
+
 cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* dout,
                                const float* lse, float* delta, float* lse2, int num_bh, int N,
                                int Npad, int D, cudaStream_t stream) {
@@ -561,13 +618,14 @@ static cudaError_t launch_bwd(K kern, int smem, int grid, const CUtensorMap& q,
 // 128-row boxes).  k/v: 64-row boxes.
 cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CUtensorMap& dout,
                                 const CUtensorMap& k, const CUtensorMap& v, const void* items,
-                                int num_items, const void* entries, const float* lse2,
-                                const float* delta, __nv_bfloat16* g0, __nv_bfloat16* g1, int N,
-                                int Npad, int hpg, float scale, int num_sms, cudaStream_t stream) {
-    if (num_items == 0) return cudaSuccess;
+                                const int* sched, int grid, const void* entries,
+                                const float* lse2, const float* delta, __nv_bfloat16* g0,
+                                __nv_bfloat16* g1, int N, int Npad, int hpg, float scale,
+                                cudaStream_t stream) {
+    if (grid == 0) return cudaSuccess;
     const float sl2 = scale * 1.4426950408889634f;
-    BwdParams pp{items, num_items, entries, lse2, delta, g0, g1, N, Npad, hpg, sl2, scale};
-    const int grid = num_items < num_sms ? num_items : num_sms;
+    BwdParams pp{items, sched, entries, lse2, delta, g0, g1, N, Npad, hpg, sl2, scale, g_trace, g_debug};
+    if (g_debug & 4) grid = 1;  // debug: isolate one CTA from memory-system contention
     if (D == 128)
         return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<128>, BwdCfg<128>::kDkvSmem, grid, q, dout, k, v, pp, stream)
                           : launch_bwd(s2_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmem, grid, q, dout, k, v, pp, stream);

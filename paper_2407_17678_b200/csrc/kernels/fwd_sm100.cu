@@ -42,7 +42,7 @@ struct PairStep {
 
 struct Fwd2Params {
     const PairItem* items;
-    int num_items;
+    const int* sched;  // [grid + 1] item range of each CTA (host-side schedule)
     const PairStep* steps;
     __nv_bfloat16* out;
     float* lse;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(384, 1)
             tma_prefetch(&tmV);
             const uint64_t keep = policy_evict_last();
             uint32_t kv_it = 0, q_use[2] = {0, 0};
-            for (int i = blockIdx.x; i < p.num_items; i += gridDim.x) {
+            for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i) {
                 const PairItem it = p.items[i];
                 const int kvbh = it.bh / p.hpg;
                 for (int t = 0; t < 2; ++t) {
@@ -169,13 +169,12 @@ __global__ void __launch_bounds__(384, 1)
             constexpr uint32_t idS64 = umma_idesc_bf16(128, 64, 0, 0);
             constexpr uint32_t idO = umma_idesc_bf16(128, D, 0, 1);
             uint32_t kv_it = 0, q_use[2] = {0, 0}, p_cnt[2] = {0, 0}, o_use[2] = {0, 0};
-            for (int i = blockIdx.x; i < p.num_items; i += gridDim.x) {
+            for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i) {
                 const PairItem it = p.items[i];
                 const PairStep* steps = p.steps + it.step_off;
                 const bool has[2] = {true, it.has_b != 0};
                 for (int t = 0; t < 2; ++t)
                     if (has[t]) mbar_wait(smem_u32(&bar_qf[t]), q_use[t] & 1);
-                tc_fence_after();
                 int pend[2] = {-1, -1};     // step whose P awaits its PV
                 int pend_half[2] = {0, 0};  // 0: both halves, 1: half 0 only, 2: half 1 only
                 bool first_pv[2] = {true, true};
@@ -197,7 +196,7 @@ __global__ void __launch_bounds__(384, 1)
                             ++p_cnt[t];
                             if (first_pv[t] && o_use[t] > 0)
                                 mbar_wait(smem_u32(&bar_oe[t]), (o_use[t] - 1) & 1);
-                            tc_fence_after();
+                            tc_fence_after();  // P was written to TMEM by tcgen05.st
                             const uint32_t sV = sKV + sm * C::kStageBytes + C::kKBytes +
                                                 (pend_half[t] == 2 ? 8192u : 0u);
                             const int nk = pend_half[t] == 0 ? 8 : 4;
@@ -213,7 +212,6 @@ __global__ void __launch_bounds__(384, 1)
                             if (m0 | m1) {
                                 if (!k_ready) {
                                     mbar_wait(smem_u32(&bar_kf[st]), ((kv_it + n) / NST) & 1);
-                                    tc_fence_after();
                                     k_ready = true;
                                 }
                                 const int half = (m0 && m1) ? 0 : (m0 ? 1 : 2);
@@ -254,7 +252,7 @@ __global__ void __launch_bounds__(384, 1)
         const int rg = r >> 4;
         const float sl2 = p.scale_log2;
         uint32_t s_cnt = 0, o_cnt = 0;
-        for (int i = blockIdx.x; i < p.num_items; i += gridDim.x) {
+        for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i) {
             const PairItem it = p.items[i];
             if (t == 1 && !it.has_b) continue;
             const PairStep* steps = p.steps + it.step_off;
@@ -394,16 +392,15 @@ static cudaError_t launch(const CUtensorMap& q, const CUtensorMap& k, const CUte
 
 }  // namespace s2dev
 
-// Host entry used by capi.cpp.  items sorted by cost (descending); grid <= #SMs.
+// Host entry used by capi.cpp: items grouped per CTA, sched = [grid + 1] offsets.
 cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtensorMap& k,
-                                const CUtensorMap& v, const void* items, int num_items,
-                                const void* steps, __nv_bfloat16* out, float* lse, int seq_len,
-                                int hpg, float scale_log2, int num_sms, cudaStream_t stream) {
-    if (num_items == 0) return cudaSuccess;
-    s2dev::Fwd2Params p{static_cast<const s2dev::PairItem*>(items), num_items,
+                                const CUtensorMap& v, const void* items, const int* sched,
+                                int grid, const void* steps, __nv_bfloat16* out, float* lse,
+                                int seq_len, int hpg, float scale_log2, cudaStream_t stream) {
+    if (grid == 0) return cudaSuccess;
+    s2dev::Fwd2Params p{static_cast<const s2dev::PairItem*>(items), sched,
                         static_cast<const s2dev::PairStep*>(steps), out, lse, seq_len, hpg,
                         scale_log2};
-    const int grid = num_items < num_sms ? num_items : num_sms;
     if (head_dim == 128) return s2dev::launch<128>(q, k, v, p, grid, stream);
     if (head_dim == 64) return s2dev::launch<64>(q, k, v, p, grid, stream);
     return cudaErrorInvalidValue;

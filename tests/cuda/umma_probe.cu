@@ -171,3 +171,208 @@ extern "C" int probe_ts(const float* P, const void* V, int KK, int Dv, float* O)
         return 1;
     }
 }
+
+// ---- throughput probe: back-to-back MMAs on resident operands -------------
+// kind 0: SS  (A smem K-major 128 x 64, B smem K-major N x 64)
+// kind 1: TS  (A tmem, B smem MN-major 16 x N rows)
+__global__ void __launch_bounds__(128, 1) probe_rate_kernel(int kind, int N, int iters, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid / 32;
+    for (int i = tid; i < 65536 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar), 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(smem_u32(&tmem_base_s), 512);
+        tmem_relinquish();
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = tmem_base_s;
+    if (tid == 0) {
+        const uint32_t sA = smem_u32(smem), sB = sA + 32768;
+        const long long t0 = clock64();
+        if (kind == 0) {
+            const uint32_t id = umma_idesc_bf16(128, N, 0, 0);
+            for (int i = 0; i < iters; ++i) {
+                const int kk = i & 3;
+                mma_ss(tb, umma_desc_sw128(sA + kk * 32, 16, 1024), umma_desc_sw128(sB + kk * 32, 16, 1024), id, 1);
+            }
+        } else {
+            const uint32_t id = umma_idesc_bf16(128, N, 0, 1);
+            for (int i = 0; i < iters; ++i) {
+                const int kk = i & 3;
+                mma_ts(tb, tb + 256 + kk * 8, umma_desc_sw128(sB + kk * 2048, 8192, 1024), id, 1);
+            }
+        }
+        const long long t1 = clock64();
+        mma_commit(smem_u32(&bar));
+        mbar_wait(smem_u32(&bar), 0);
+        const long long t2 = clock64();
+        out[0] = t1 - t0;
+        out[1] = t2 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tb, 512);
+}
+
+extern "C" int probe_rate(int kind, int N, int iters, long long* host_out) {
+    long long* d;
+    cudaMalloc(&d, 16);
+    const int smem = 1024 + 65536;
+    cudaFuncSetAttribute(probe_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    probe_rate_kernel<<<1, 128, smem>>>(kind, N, iters, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(host_out, d, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) {
+        snprintf(g_msg, sizeof g_msg, "%s", cudaGetErrorString(e));
+        return 2;
+    }
+    return 0;
+}
+
+__device__ __forceinline__ bool lane_is_zero() { return (threadIdx.x & 31) == 0; }
+
+// ---- the dK/dV step's MMA sequence alone (no TMA, no elementwise) ----------
+// per step: S^T (SS N=64 x 8), dP^T (SS N=64 x 8), dV (TS N=128 x 4), dK (TS N=128 x 4)
+__global__ void __launch_bounds__(256, 1) probe_dkv_seq_kernel(int steps, int variant, long long* out, const uint8_t* gsrc) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar, bar2[2];
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid / 32;
+    for (int i = tid; i < 131072 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar2[0]), 1);
+        mbar_init(smem_u32(&bar2[1]), 1);
+        mbar_init(smem_u32(&bar), 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(smem_u32(&tmem_base_s), 512);
+        tmem_relinquish();
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = tmem_base_s;
+    if (tid == 0) {
+        const uint32_t sK0 = smem_u32(smem);
+        const uint32_t idS = umma_idesc_bf16(128, 64, 0, 0), idA = umma_idesc_bf16(128, 128, 0, 1);
+        const long long t0 = clock64();
+        for (int n = 0; n < steps; ++n) {
+            const int b = n & 1;
+            const uint32_t sK = sK0, sV = sK0 + 32768;
+            const uint32_t rot = variant == 11 ? (n % 2) * 32768 : 0;  // rotate Q/dO stage
+            const uint32_t sQ = sK0 + 65536 + rot - (variant == 11 ? 0 : 0), sdO = sQ + 16384;
+            if (variant != 2) {
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int sub = kk >> 2, off = (kk & 3) * 32;
+                    mma_ss(tb + b * 64, umma_desc_sw128(sK + sub * 16384 + off, 16, 1024),
+                           umma_desc_sw128(sQ + sub * 8192 + off, 16, 1024), idS, kk > 0);
+                    mma_ss(tb + 128 + b * 64, umma_desc_sw128(sV + sub * 16384 + off, 16, 1024),
+                           umma_desc_sw128(sdO + sub * 8192 + off, 16, 1024), idS, kk > 0);
+                }
+            }
+            if (variant == 7 || variant == 8) mma_commit(smem_u32(&bar2[0]));
+            if (variant == 9) tc_fence_after();
+            if (variant == 10) {
+                mma_commit(smem_u32(&bar2[0]));
+                mbar_wait(smem_u32(&bar2[0]), n & 1);  // wait for the group, like waiting S before PV
+                tc_fence_after();
+            }
+            if (variant != 1) {
+                for (int kk = 0; kk < 4; ++kk) {
+                    mma_ts(tb + 256, tb + b * 64 + kk * 8, umma_desc_sw128(sdO + kk * 2048, 8192, 1024), idA, 1);
+                    mma_ts(tb + 384, tb + 128 + b * 64 + kk * 8, umma_desc_sw128(sQ + kk * 2048, 8192, 1024), idA, 1);
+                }
+            }
+            if (variant == 8) mma_commit(smem_u32(&bar2[1]));
+        }
+        mma_commit(smem_u32(&bar));
+        mbar_wait(smem_u32(&bar), 0);
+        out[0] = clock64() - t0;
+        atomicExch(reinterpret_cast<int*>(&tmem_base_s) + 0, tb);  // keep
+        *reinterpret_cast<volatile int*>(out + 1) = 1;  // done flag
+    }
+    if (warp == 4 && variant == 5 && lane_is_zero()) {
+        // contention: TMA bulk copies of 32 KB per ~1000 cycles into a spare region
+        __shared__ uint64_t tbar;
+        mbar_init(smem_u32(&tbar), 1);
+        fence_mbar_init();
+        const uint32_t dst = smem_u32(smem) + 131072 - 32768;
+        uint32_t ph = 0;
+        int it = 0;
+        while (*reinterpret_cast<volatile int*>(out + 1) == 0 && it < 100000) {
+            mbar_expect_tx(smem_u32(&tbar), 32768);
+            for (int c = 0; c < 4; ++c)
+                bulk_load(dst + c * 8192, gsrc + (static_cast<size_t>(it % 64) * 32768) + c * 8192, 8192, smem_u32(&tbar));
+            mbar_wait(smem_u32(&tbar), ph);
+            ph ^= 1;
+            ++it;
+        }
+    }
+    if (warp >= 1 && variant == 6) {
+        // issue contention: every other warp runs an FMA/MUFU mix until done
+        float a = threadIdx.x * 1e-3f, b = 1.0001f, c = 0.f;
+        int it = 0;
+        while (*reinterpret_cast<volatile int*>(out + 1) == 0 && it < 2000000) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                a = fmaf(a, b, 1e-7f);
+                c += fast_exp2(a);
+            }
+            ++it;
+        }
+        if (c == 12345.f) out[2] = 1;
+    }
+    if (warp >= 4 && variant >= 3 && variant <= 4) {
+        // contention: load S^T/dP^T-sized chunks and store P-sized chunks like the elementwise WG
+        const uint32_t lo = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        uint32_t r[32];
+        int it = 0;
+        while (*reinterpret_cast<volatile int*>(out + 1) == 0 && it < 200000) {
+            tmem_ld32(tb + lo + (it & 1) * 64, r);
+            tmem_ld32(tb + lo + 128 + (it & 1) * 64, r);
+            tmem_ld_wait();
+            if (variant == 4) {
+                uint32_t w[16];
+                for (int j = 0; j < 16; ++j) w[j] = r[j] + 1;
+                tmem_st16(tb + lo + 200, w);
+                tmem_st_wait();
+            }
+            ++it;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tb, 512);
+}
+
+__device__ __forceinline__ bool lane_is_zero_dummy() { return true; }
+extern "C" int probe_dkv_seq(int steps, int variant, long long* host_out) {
+    long long* d;
+    cudaMalloc(&d, 32);
+    static uint8_t* gsrc = nullptr;
+    if (!gsrc) {
+        cudaMalloc(&gsrc, 64 * 32768);
+        cudaMemset(gsrc, 0, 64 * 32768);
+    }
+    const int smem = 1024 + 131072;
+    cudaFuncSetAttribute(probe_dkv_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaMemset(d, 0, 32);
+    probe_dkv_seq_kernel<<<1, 256, smem>>>(steps, variant, d, gsrc);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(host_out, d, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? 0 : 2;
+}

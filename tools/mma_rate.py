@@ -1,0 +1,18 @@
+"""Measure tcgen05.mma throughput per shape on one SM (probe library)."""
+import ctypes, os, subprocess, sys
+HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+so = os.path.join(HERE, "tests", "cuda", "libumma_probe.so")
+subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+                       "-Xcompiler", "-fPIC", "-shared", "-o", so, os.path.join(HERE, "tests", "cuda", "umma_probe.cu")])
+L = ctypes.CDLL(so)
+out = (ctypes.c_longlong * 2)()
+for kind, name in ((0, "SS"), (1, "TS")):
+    for N in (64, 128, 256):
+        iters = 4096
+        assert L.probe_rate(kind, N, iters, out) == 0
+        cyc = out[1] / iters
+        ideal = 128 * N / 256
+        print(f"{name} M=128 N={N:3d} K=16: {cyc:6.1f} cyc/MMA (issue {out[0]/iters:5.1f}), ideal {ideal:5.1f} -> {ideal/cyc:.0%}")
+for variant, name in ((0, "S,dP + dV,dK"), (1, "S,dP only"), (2, "dV,dK only"), (3, "all + concurrent TMEM loads"), (4, "all + concurrent TMEM ld+st"), (5, "all + concurrent TMA 32KB loads"), (6, "all + 7 ALU-busy warps (issuer = lowest wid)"), (7, "commit after S,dP"), (8, "commit after S,dP and after dV,dK"), (9, "fence::after_thread_sync between groups"), (10, "commit+wait+fence between groups (drain)"), (11, "Q/dO tiles rotate between 2 stages")):
+    assert L.probe_dkv_seq(512, variant, out) == 0
+    print(f"dkv step sequence [{name}]: {out[0]/512:.0f} cyc/step")
