@@ -7,6 +7,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <unordered_map>
 
 #include "capi_internal.hpp"
 #include "tma_host.hpp"
@@ -119,15 +120,24 @@ Lists* get_lists(s2_plan* p, int seq_len, int* status) {
     return L;
 }
 
-// Static persistent-CTA schedule: items are visited in `order` (head-major,
-// heaviest first inside a head) and each goes to the CTA whose queue
-// finishes earliest (greedy list scheduling).  CTAs therefore sweep the
-// heads together — a head's K/V (or Q/dO) stays L2-resident while every CTA
-// works on it — and the tail is made of the lightest items.  Returns the
+// Static persistent-CTA schedule (greedy list scheduling: each item goes to
+// the CTA whose queue finishes earliest).  Items are visited in cost
+// classes, heaviest class first (LPT: the tail is made of the lightest
+// items), and head-major inside a class, so CTAs sweep the heads of one class
+// together and a head's K/V (or Q/dO) stays L2-resident while they do.  A
+// class spans a factor of 2^(1/4) in cost.  `overhead` is the fixed per-item
+// cost (operand loads, epilogue) in the same unit as `cost`.  Returns the
 // items regrouped per CTA plus offsets [grid + 1].
 template <class T, class Cost, class Key>
-static std::vector<int32_t> schedule_items(std::vector<T>& items, int grid, Cost cost, Key key) {
+static std::vector<int32_t> schedule_items(std::vector<T>& items, int grid, Cost cost, Key key,
+                                           int64_t overhead) {
+    auto cls = [&](const T& a) {
+        const double c = static_cast<double>(cost(a) + overhead);
+        return static_cast<int>(std::floor(4.0 * std::log2(std::max(1.0, c))));
+    };
     std::stable_sort(items.begin(), items.end(), [&](const T& a, const T& b) {
+        const int ca = cls(a), cb = cls(b);
+        if (ca != cb) return ca > cb;
         const auto ka = key(a), kb = key(b);
         if (ka != kb) return ka < kb;
         return cost(a) > cost(b);
@@ -140,7 +150,7 @@ static std::vector<int32_t> schedule_items(std::vector<T>& items, int grid, Cost
         std::pop_heap(heap.begin(), heap.end(), std::greater<>());
         auto& top = heap.back();
         per[top.second].push_back(it);
-        top.first += cost(it) + 4;  // + fixed per-item overhead
+        top.first += cost(it) + overhead;
         std::push_heap(heap.begin(), heap.end(), std::greater<>());
     }
     std::vector<int32_t> off(grid + 1, 0);
@@ -202,7 +212,7 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
         const int grid = num_sms();
         const std::vector<int32_t> off_fwd = schedule_items(
             fi, grid, [](const s2dev::FwdItem& a) { return int64_t(a.chunk_cnt); },
-            [](const s2dev::FwdItem& a) { return a.bh; });
+            [](const s2dev::FwdItem& a) { return a.bh; }, 2);
         struct PairItem {
             int32_t bh, qpair, nsteps, has_b;
             int64_t step_off;
@@ -218,7 +228,7 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
             }
         const std::vector<int32_t> off_pair = schedule_items(
             pi, grid, [](const PairItem& a) { return int64_t(a.nsteps) * (1 + a.has_b); },
-            [](const PairItem& a) { return a.bh; });
+            [](const PairItem& a) { return a.bh; }, 4);
         w->num_pair = static_cast<int>(pi.size());
         if ((e = upload(w->pair, pi.data(), pi.size() * sizeof(PairItem))) != cudaSuccess ||
             (e = upload(w->pair_sched, off_pair.data(), off_pair.size() * sizeof(int32_t))) != cudaSuccess ||
@@ -232,9 +242,21 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
             for (const BwdTile& t : L->bwd.tiles)
                 if (t.group == g) bi.push_back({static_cast<int>(ui), t.c0, t.c1, t.count, t.offset});
         }
+        // dK/dV cost: 64-row q halves the kernel steps through (a half with
+        // no mask bit in either chunk is skipped) for every head of the group.
+        std::unordered_map<int64_t, int64_t> halves;  // tile entry offset -> active halves
+        for (const BwdTile& t : L->bwd.tiles) {
+            int64_t h = 0;
+            for (int e = 0; e < t.count; ++e) {
+                const BwdEntry& en = L->bwd.entries[t.offset + e];
+                const uint32_t m = en.mask0 | en.mask1;
+                h += ((m & 0xFFFFu) != 0) + ((m >> 16) != 0);
+            }
+            halves[t.offset] = h;
+        }
+        auto bwd_cost = [&halves, hpg](const s2dev::BwdItem& a) { return halves.at(a.offset) * hpg; };
         const std::vector<int32_t> off_bwd = schedule_items(
-            bi, grid, [hpg](const s2dev::BwdItem& a) { return int64_t(a.count) * hpg; },
-            [](const s2dev::BwdItem& a) { return a.kvbh; });
+            bi, grid, bwd_cost, [](const s2dev::BwdItem& a) { return a.kvbh; }, 4);
         w->num_fwd = static_cast<int>(fi.size());
         w->num_bwd = static_cast<int>(bi.size());
         w->grid = grid;
