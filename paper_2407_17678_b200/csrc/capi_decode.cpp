@@ -57,12 +57,26 @@ int64_t retained_tokens(const s2_kvcache* c, int g) {
     for (int64_t i = a; i < b; ++i) n += c->row_blocks[i] < bt ? c->S : (t - bt * c->S + 1);
     return n;
 }
+// Split-KV factor: every split CTA streams about the same number of blocks,
+// so the launch runs in waves of 2 CTAs / SM.  Take the smallest split
+// count giving at least two waves whose last wave is >= 95% full (else the
+// fullest), keeping >= 4 blocks per split.
 int choose_splits(const s2_kvcache* c, int max_len) {
-    const int units = c->batch * c->Hkv;
-    const int target = 4 * 2 * num_sms();  // ~4 waves at 2 CTAs / SM
-    int s = (target + units - 1) / units;
-    s = std::max(1, std::min({s, kMaxSplits, std::max(1, max_len / 4)}));
-    return s;
+    const double units = static_cast<double>(c->batch) * c->Hkv;
+    const double slots = 2.0 * num_sms();
+    const int s_max = std::max(1, std::min(kMaxSplits, max_len / 4));
+    int best = 1;
+    double best_eff = -1.0;
+    for (int s = 1; s <= s_max; ++s) {
+        const double waves = units * s / slots;
+        const double eff = waves / std::ceil(waves);
+        if (waves >= 2.0 && eff >= 0.95) return s;
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = s;
+        }
+    }
+    return best;
 }
 }  // namespace
 

@@ -12,9 +12,10 @@
 //  * s2_kv_append_kernel:  one new token per (b, kv head)
 //  * s2_decode_split_kernel: split-KV attention of all query heads of a GQA
 //    group at position t over a contiguous range of the row's slots; K/V
-//    64-token blocks streamed by TMA (128-byte swizzle, conflict-free smem
-//    reads) through an NST-deep ring; fp32 math on CUDA cores (the step is
-//    HBM-bound: ~0.25 FMA/byte); partial (o, lse) per split.
+//    64-token blocks streamed by TMA (128-byte swizzle) through an NST-deep
+//    ring by a producer warp; QK^T and PV on the tensor cores (mma.sync, the
+//    group's heads as the M rows), fp32 online softmax; partial (o, lse) per
+//    split.
 //  * s2_decode_combine_kernel: lse-weighted merge of the splits.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -25,21 +26,55 @@
 namespace s2dev {
 
 
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+// D(16x8, f32) += A(16x16, bf16, rows 8..15 zero) * B(16x8, bf16)
+__device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0,
+                                          uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+        "{%8, %9}, {%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+// Split-KV decode of one (batch, kv head, split).  Warp 4 streams the
+// split's 64-token K/V blocks by TMA (128-byte swizzle) through an NST ring;
+// warps 0-3 each own 16 tokens of every block and run the block on the
+// tensor cores (mma.sync m16n8k16: the GQA group's query heads are the M
+// rows, so one K/V read serves every head of the group):
+//   S(heads x 16 tok) = Q K^T   (K fragments by ldmatrix)
+//   P = exp2(S*scale - m)        online softmax per warp (quad shuffles)
+//   O(heads x D) += P V          (P re-used from the S accumulators as the A
+//                                 fragment; V fragments by ldmatrix.trans)
+// The four per-warp states (m, l, O) are merged through shared memory and
+// written as the split's partial (o, lse); s2_decode_combine_kernel merges
+// the splits.  The step is HBM-bound; the MMAs only keep the SM's issue
+// slots free so the ring stays full.
 template <int HPG, int D>
-__global__ void __launch_bounds__(128) s2_decode_split_kernel(const __grid_constant__ CUtensorMap tmK,
+__global__ void __launch_bounds__(160) s2_decode_split_kernel(const __grid_constant__ CUtensorMap tmK,
                                                               const __grid_constant__ CUtensorMap tmV,
                                                               const DecodeParams p) {
     constexpr int NST = 3;
     constexpr int SUB = D / 64;
     constexpr int BLK_BYTES = SUB * 8192;  // 64 tokens x D bf16
+    constexpr int KSTEPS = D / 16;
+    constexpr int NT = D / 8;  // n-tiles of the PV product
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_full[NST];
-    __shared__ float sq[HPG][D];           // q of the group's heads, pre-scaled (log2)
-    __shared__ float sp[HPG][64];          // probabilities of the current block
-    __shared__ float smax[2][HPG];
-    const int tid = threadIdx.x;
+    __shared__ uint64_t bar_full[NST], bar_empty[NST];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
     const int64_t roff = p.row_ptr[static_cast<size_t>(g) * (p.NB + 1) + p.bt];
     const int len = static_cast<int>(p.row_ptr[static_cast<size_t>(g) * (p.NB + 1) + p.bt + 1] - roff);
@@ -47,155 +82,157 @@ __global__ void __launch_bounds__(128) s2_decode_split_kernel(const __grid_const
     const int nblk = max(0, min(p.blocks_per_split, len - first));
     const int* slots = p.slot_idx + roff + first;
     const int kvbh = b * p.Hkv + g;
+    const uint32_t sbase = smem_u32(smem);
 
-    for (int i = tid; i < HPG * D; i += 128) {
-        const int h = i / D, x = i % D;
-        sq[h][x] = __bfloat162float(p.q[(static_cast<size_t>(b) * p.H + g * HPG + h) * D + x]) *
-                   p.scale_log2;
-    }
     if (tid == 0) {
-        for (int i = 0; i < NST; ++i) mbar_init(smem_u32(&bar_full[i]), 1);
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(smem_u32(&bar_full[i]), 1);
+            mbar_init(smem_u32(&bar_empty[i]), 4);
+        }
         fence_mbar_init();
     }
     __syncthreads();
-    const uint32_t sbase = smem_u32(smem);
-    auto issue = [&](int i) {
-        const int st = i % NST;
-        const uint32_t dst = sbase + st * 2 * BLK_BYTES;
-        const uint32_t bar = smem_u32(&bar_full[st]);
-        mbar_expect_tx(bar, 2 * BLK_BYTES);
-        const int row = slots[i] * 64;
-#pragma unroll
-        for (int s = 0; s < SUB; ++s) {
-            tma_load_3d(dst + s * 8192, &tmK, bar, s * 64, row, kvbh);
-            tma_load_3d(dst + BLK_BYTES + s * 8192, &tmV, bar, s * 64, row, kvbh);
-        }
-    };
-    if (tid == 0)
-        for (int i = 0; i < NST && i < nblk; ++i) issue(i);
 
-    // score mapping: token = tid % 64, heads hs*NHT .. of hs = tid / 64
-    constexpr int NHT = HPG >= 2 ? HPG / 2 : 1;
-    const int tok = tid & 63, hs = tid >> 6;
-    const bool score_thread = HPG >= 2 || hs == 0;
-    // PV mapping: 16-byte d-chunk c = tid % (D/8), token group tg = tid / (D/8)
-    constexpr int NCH = D / 8;             // 16B chunks per row
-    constexpr int NTG = 128 / NCH;         // token groups
-    const int c = tid % NCH, tg = tid / NCH;
-    float acc[HPG][8];
+    if (warp == 4) {
+        // ---------------------------------------------------------- producer
+        if (lane == 0) {
+            const uint64_t stream = policy_evict_first();
+            for (int i = 0; i < nblk; ++i) {
+                const int st = i % NST;
+                if (i >= NST) mbar_wait(smem_u32(&bar_empty[st]), ((i / NST) + 1) & 1);
+                const uint32_t dst = sbase + st * 2 * BLK_BYTES;
+                const uint32_t bar = smem_u32(&bar_full[st]);
+                mbar_expect_tx(bar, 2 * BLK_BYTES);
+                const int row = slots[i] * 64;
 #pragma unroll
-    for (int h = 0; h < HPG; ++h)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[h][e] = 0.f;
-    float m_run[HPG], l_run[HPG];
-#pragma unroll
-    for (int h = 0; h < HPG; ++h) {
-        m_run[h] = -INFINITY;
-        l_run[h] = 0.f;
+                for (int s = 0; s < SUB; ++s) {
+                    tma_load_3d_hint(dst + s * 8192, &tmK, bar, s * 64, row, kvbh, stream);
+                    tma_load_3d_hint(dst + BLK_BYTES + s * 8192, &tmV, bar, s * 64, row, kvbh, stream);
+                }
+            }
+        }
+        return;
     }
+
+    // -------------------------------------------------------------- consumers
+    const int gq = lane >> 2, tg = lane & 3;  // fragment row (head) / column pair
+    const bool head_ok = gq < HPG;
+    // A fragments of Q (rows = heads, rows 8..15 are zero): a0 = cols 2tg.., a2 = cols 2tg+8..
+    uint32_t qa[KSTEPS][2];
+    {
+        const __nv_bfloat16* qrow = p.q + (static_cast<size_t>(b) * p.H + g * HPG + (head_ok ? gq : 0)) * D;
+#pragma unroll
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+            qa[kk][0] = head_ok ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * tg) : 0u;
+            qa[kk][1] = head_ok ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * tg) : 0u;
+        }
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+    const float sl2 = p.scale_log2;
+    const int tok0 = warp * 16;  // this warp's tokens within each block
+    // ldmatrix row addresses (swizzled: 16-byte chunk c of token r sits at c ^ (r & 7))
+    const int mi = lane >> 3, r8 = lane & 7;
+    const int k_tok = tok0 + (mi >> 1) * 8 + r8, k_chk = mi & 1;   // K: {n-tile, k-half}
+    const int v_tok = tok0 + (mi & 1) * 8 + r8, v_chk = mi >> 1;   // V: {k-half, n-tile}
 
     for (int i = 0; i < nblk; ++i) {
         const int st = i % NST;
         mbar_wait(smem_u32(&bar_full[st]), (i / NST) & 1);
-        const uint8_t* sK = smem + st * 2 * BLK_BYTES;
-        const uint8_t* sV = sK + BLK_BYTES;
+        const uint32_t sK = sbase + st * 2 * BLK_BYTES, sV = sK + BLK_BYTES;
         const int valid = (first + i == len - 1) ? p.last_tokens : 64;
-        // ---- scores
-        float s[NHT];
+        // ---- S = Q K^T for 16 tokens (two n-tiles)
+        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-        for (int h = 0; h < NHT; ++h) s[h] = 0.f;
-        if (score_thread) {
-#pragma unroll
-            for (int sub = 0; sub < SUB; ++sub)
-#pragma unroll
-                for (int ch = 0; ch < 8; ++ch) {
-                    const uint4 kv = *reinterpret_cast<const uint4*>(
-                        sK + sub * 8192 + tok * 128 + ((ch ^ (tok & 7)) << 4));
-                    const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv);
-                    float kf[8];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        kf[2 * e] = __low2float(k2[e]);
-                        kf[2 * e + 1] = __high2float(k2[e]);
-                    }
-                    const int x0 = sub * 64 + ch * 8;
-#pragma unroll
-                    for (int h = 0; h < NHT; ++h) {
-                        const float* qh = sq[hs * NHT + h] + x0;
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) s[h] = fmaf(qh[e], kf[e], s[h]);
-                    }
-                }
-            if (tok >= valid)
-#pragma unroll
-                for (int h = 0; h < NHT; ++h) s[h] = -INFINITY;
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+            const int c = 2 * kk + k_chk;  // 16-byte chunk along D
+            const uint32_t addr = sK + (c >> 3) * 8192 + k_tok * 128 + (((c & 7) ^ (k_tok & 7)) << 4);
+            uint32_t b00, b01, b10, b11;
+            ldsm_x4(addr, b00, b01, b10, b11);
+            mma_16816(sc[0], qa[kk][0], qa[kk][1], b00, b01);
+            mma_16816(sc[1], qa[kk][0], qa[kk][1], b10, b11);
         }
-        // ---- block max per head (two warps per head set)
-#pragma unroll
-        for (int h = 0; h < NHT; ++h) {
-            float mx = s[h];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            if ((tid & 31) == 0 && score_thread) smax[(tid >> 5) & 1][hs * NHT + h] = mx;
+        // ---- online softmax (row = head gq; its 16 scores live in the quad)
+        float s[4] = {sc[0][0] * sl2, sc[0][1] * sl2, sc[1][0] * sl2, sc[1][1] * sl2};
+        if (valid < 64) {
+            const int t0 = tok0 + 2 * tg;
+            if (t0 >= valid) s[0] = -INFINITY;
+            if (t0 + 1 >= valid) s[1] = -INFINITY;
+            if (t0 + 8 >= valid) s[2] = -INFINITY;
+            if (t0 + 9 >= valid) s[3] = -INFINITY;
         }
-        __syncthreads();
-        float alpha[HPG];
+        float mx = fmaxf(fmaxf(s[0], s[1]), fmaxf(s[2], s[3]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run, mx);
+        const float base = m_new == -INFINITY ? 0.f : m_new;
+        const float alpha = fast_exp2(m_run - base);
+        float pr[4];
 #pragma unroll
-        for (int h = 0; h < HPG; ++h) {
-            const float mb = fmaxf(smax[0][h], smax[1][h]);
-            const float mn = fmaxf(m_run[h], mb);
-            alpha[h] = (m_run[h] == -INFINITY) ? 0.f : fast_exp2(m_run[h] - mn);
-            m_run[h] = mn;
+        for (int e = 0; e < 4; ++e) pr[e] = fast_exp2(s[e] - base);
+        l_run = l_run * alpha + (pr[0] + pr[1]) + (pr[2] + pr[3]);
+        m_run = m_new;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            o[j][0] *= alpha;
+            o[j][1] *= alpha;
         }
-        if (score_thread)
+        const uint32_t pa0 = pack_bf16(pr[0], pr[1]), pa2 = pack_bf16(pr[2], pr[3]);
+        // ---- O += P V (V fragments transposed out of the token-major tile)
 #pragma unroll
-            for (int h = 0; h < NHT; ++h) sp[hs * NHT + h][tok] = fast_exp2(s[h] - m_run[hs * NHT + h]);
-        __syncthreads();
-        // ---- l and PV
-#pragma unroll
-        for (int h = 0; h < HPG; ++h) {
-            float ps = 0.f;
-            for (int t = 0; t < 64; ++t) ps += sp[h][t];
-            l_run[h] = l_run[h] * alpha[h] + ps;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[h][e] *= alpha[h];
+        for (int j = 0; j < NT; j += 2) {
+            const int c = j + v_chk;
+            const uint32_t addr = sV + (c >> 3) * 8192 + v_tok * 128 + (((c & 7) ^ (v_tok & 7)) << 4);
+            uint32_t b0a, b1a, b0b, b1b;
+            ldsm_x4_t(addr, b0a, b1a, b0b, b1b);
+            mma_16816(o[j], pa0, pa2, b0a, b1a);
+            mma_16816(o[j + 1], pa0, pa2, b0b, b1b);
         }
-        const int sub = c / 8, ch = c % 8;
-        for (int t = tg; t < 64; t += NTG) {
-            const uint4 vv = *reinterpret_cast<const uint4*>(sV + sub * 8192 + t * 128 + ((ch ^ (t & 7)) << 4));
-            const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vv);
-            float vf[8];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                vf[2 * e] = __low2float(v2[e]);
-                vf[2 * e + 1] = __high2float(v2[e]);
-            }
-#pragma unroll
-            for (int h = 0; h < HPG; ++h) {
-                const float ph = sp[h][t];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc[h][e] = fmaf(ph, vf[e], acc[h][e]);
-            }
-        }
-        __syncthreads();
-        if (tid == 0 && i + NST < nblk) issue(i + NST);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bar_empty[st]));
     }
-    // ---- reduce the token groups through shared memory (reuse the ring)
-    float* red = reinterpret_cast<float*>(smem);  // [NTG][HPG][D]
-    __syncthreads();
+    // quad-reduce l (each lane summed its own 4 columns)
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+
+    // ---- merge the four warps' states (reuse the ring: every stage was consumed)
+    named_bar_sync(1, 128);
+    float* red_o = reinterpret_cast<float*>(smem);   // [4][HPG][D]
+    float* red_m = red_o + 4 * HPG * D;              // [4][HPG]
+    float* red_l = red_m + 4 * HPG;                  // [4][HPG]
+    if (head_ok) {
 #pragma unroll
-    for (int h = 0; h < HPG; ++h)
+        for (int j = 0; j < NT; ++j) {
+            float* dst = red_o + (warp * HPG + gq) * D + j * 8 + 2 * tg;
+            dst[0] = o[j][0];
+            dst[1] = o[j][1];
+        }
+        if (tg == 0) {
+            red_m[warp * HPG + gq] = m_run;
+            red_l[warp * HPG + gq] = l_run;
+        }
+    }
+    named_bar_sync(1, 128);
+    for (int idx = tid; idx < HPG * D; idx += 128) {
+        const int h = idx / D, x = idx % D;
+        float M = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) red[(tg * HPG + h) * D + c * 8 + e] = acc[h][e];
-    __syncthreads();
-    for (int i = tid; i < HPG * D; i += 128) {
-        const int h = i / D, x = i % D;
-        float o = 0.f;
-        for (int t = 0; t < NTG; ++t) o += red[(t * HPG + h) * D + x];
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, red_m[w * HPG + h]);
+        float num = 0.f, den = 0.f;
+        if (M != -INFINITY) {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const float f = fast_exp2(red_m[w * HPG + h] - M);
+                num += f * red_o[(w * HPG + h) * D + x];
+                den += f * red_l[w * HPG + h];
+            }
+        }
         const size_t row = (static_cast<size_t>(b) * p.H + g * HPG + h) * p.splits + split;
-        const float l = l_run[h];
-        p.o_part[row * D + x] = nblk > 0 && l > 0.f ? o / l : 0.f;
-        if (x == 0) p.lse_part[row] = nblk > 0 && l > 0.f ? m_run[h] + __log2f(l) : -INFINITY;
+        const bool ok = den > 0.f;
+        p.o_part[row * D + x] = ok ? num / den : 0.f;
+        if (x == 0) p.lse_part[row] = ok ? M + __log2f(den) : -INFINITY;
     }
 }
 
@@ -265,10 +302,11 @@ template <int HPG, int D>
 static cudaError_t launch_decode(const CUtensorMap& mk, const CUtensorMap& mv,
                                  const DecodeParams& p, int batch, cudaStream_t st) {
     const int smem = 1024 + 3 * 2 * (D / 64) * 8192;
+    static_assert(4 * HPG * D * 4 + 8 * HPG * 4 <= 3 * 2 * (D / 64) * 8192, "merge buffer fits the ring");
     auto kern = s2_decode_split_kernel<HPG, D>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<dim3(p.splits, p.Hkv, batch), 128, smem, st>>>(mk, mv, p);
+    kern<<<dim3(p.splits, p.Hkv, batch), 160, smem, st>>>(mk, mv, p);
     return cudaGetLastError();
 }
 

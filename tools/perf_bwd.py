@@ -27,6 +27,9 @@ for _ in range(3):
     s2.s2_attn_fwd(plan, q, k, v, out=out, lse=lse)
     s2.s2_attn_bwd(plan, q, k, v, out, lse, do, dq=dq, dk=dk, dv=dv)
 torch.cuda.synchronize()
+import ctypes
+L = s2.lib()
+L.s2_profile_enable(1)
 tf = tb = 0.0
 for _ in range(a.iters):
     ev[0].record()
@@ -43,3 +46,11 @@ act, dense = plan.fwd_flops(a.b, a.d)
 print(f"N={a.n} H={a.h} B={a.b}: fwd {tf:.3f} ms ({act/tf/1e9:.0f} TF/s)  bwd {tb:.3f} ms "
       f"({2.5*act/tb/1e9:.0f} TF/s)  fwd+bwd {tf+tb:.3f} ms ({3.5*act/(tf+tb)/1e9:.0f} TF/s active, "
       f"{3.5*dense/(tf+tb)/1e9:.0f} dense-equiv)")
+names = ctypes.create_string_buffer(32 * 16)
+tot = (ctypes.c_double * 16)()
+cnt = (ctypes.c_int * 16)()
+nk = ctypes.c_int()
+L.s2_profile_collect(16, names, tot, cnt, ctypes.byref(nk))
+L.s2_profile_enable(0)
+print("  kernels: " + ", ".join(
+    f"{names.raw[32*i:32*i+32].split(b'\\0')[0].decode()} {tot[i]/cnt[i]:.3f} ms" for i in range(nk.value)))
