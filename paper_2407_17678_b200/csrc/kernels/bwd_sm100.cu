@@ -185,13 +185,24 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
             }
-        } else if (warp == 1 && lane == 0) {
+        } else if (warp == 1) {
             // ---------------------------------------------------- MMA issuer
+            // The whole warp runs the loop on warp-uniform values; one elected
+            // lane issues (keeps descriptors in uniform registers: no
+            // per-MMA waterfall loop).
             constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);
             constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
+            const bool leader = elect_one();
+            // descriptor of the K / V tiles and of stage 0's Q / dO tiles; SW128
+            // K-major advance along K = +32 B per 16 elements (+2 in the desc)
+            const uint64_t dK0 = umma_desc_sw128(sK, 16, 1024), dV0 = umma_desc_sw128(sV, 16, 1024);
+            const uint64_t dSt0 = umma_desc_sw128(sSt, 16, 1024);
+            const uint64_t dStMN0 = umma_desc_sw128(sSt, 8192, 1024);
             uint32_t it_cnt = 0, st_it = 0, n_glob = 0;
-            for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
-                const BwdItem it = items[i];
+            const int i_end = p.sched[blockIdx.x + 1];
+            for (int i = p.sched[blockIdx.x]; i < i_end; ++i, ++it_cnt) {
+                const int offset = warp_uniform(static_cast<int>(items[i].offset));
+                const int count = warp_uniform(items[i].count);
                 mbar_wait(smem_u32(&bar_kvf), it_cnt & 1);
                 bool first = true;
                 int prev_st = -1;
@@ -203,42 +214,47 @@ __global__ void __launch_bounds__(384, 1)
                     S2TRACE(4, n);
                     if (first && it_cnt > 0) mbar_wait(smem_u32(&bar_ae), (it_cnt - 1) & 1);
                     tc_fence_after();  // A operands (P^T, dS^T) were written to TMEM by tcgen05.st
-                    const uint32_t base = sSt + st * C::kDkvStage;
+                    const uint64_t dst = dStMN0 + static_cast<uint64_t>((st * C::kDkvStage) >> 4);
+                    if (leader) {
 #pragma unroll
-                    for (int kk = 0; kk < ((p.debug & 2) ? 0 : 4); ++kk) {
-                        const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-                        // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
-                        mma_ts(tmem + 256, tmem + b * 64 + kk * 8,
-                               umma_desc_sw128(base + C::kTile64 + kk * 2048, 8192, 1024), idA, acc);
-                        mma_ts(tmem + 384, tmem + 128 + b * 64 + kk * 8,
-                               umma_desc_sw128(base + kk * 2048, 8192, 1024), idA, acc);
+                        for (int kk = 0; kk < ((p.debug & 2) ? 0 : 4); ++kk) {
+                            const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+                            // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
+                            // K slice kk of P^T / dS^T: WG (kk >> 1) stored it at 32*(kk>>1) + 8*(kk&1)
+                            const uint32_t ac = b * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                            mma_ts(tmem + 256, tmem + ac, dst + ((C::kTile64 + kk * 2048) >> 4), idA, acc);
+                            mma_ts(tmem + 384, tmem + 128 + ac, dst + ((kk * 2048) >> 4), idA, acc);
+                        }
+                        mma_commit(smem_u32(&bar_se[st]));
                     }
+                    __syncwarp();
                     first = false;
-                    mma_commit(smem_u32(&bar_se[st]));
                 };
                 for (int j = 0; j < p.hpg; ++j)
-                    for (int e = 0; e < it.count; ++e) {
-                        const BwdEntry en = ents[it.offset + e];
+                    for (int e = 0; e < count; ++e) {
+                        const BwdEntry en = ents[offset + e];
+                        const uint32_t mor = warp_uniform(en.mask0 | en.mask1);
                         for (int half = 0; half < 2; ++half) {
-                            if (!half_active(en, half)) continue;
+                            if (((mor >> (16 * half)) & 0xFFFFu) == 0) continue;
                             const int st = st_it % NST;
                             S2TRACE(0, n_glob);
                             mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
                             S2TRACE(1, n_glob);
-                            const uint32_t base = sSt + st * C::kDkvStage;
+                            const uint64_t dst = dSt0 + static_cast<uint64_t>((st * C::kDkvStage) >> 4);
                             const int b = n_glob & 1;
+                            if (leader) {
 #pragma unroll
-                            for (int kk = 0; kk < D / 16; ++kk) {
-                                const int sub = kk >> 2, off = (kk & 3) * 32;
-                                // S^T = K Q^T ; dP^T = V dO^T  (K-major x K-major)
-                                mma_ss(tmem + b * 64, umma_desc_sw128(sK + sub * 16384 + off, 16, 1024),
-                                       umma_desc_sw128(base + sub * 8192 + off, 16, 1024), idS, kk > 0);
-                                mma_ss(tmem + 128 + b * 64,
-                                       umma_desc_sw128(sV + sub * 16384 + off, 16, 1024),
-                                       umma_desc_sw128(base + C::kTile64 + sub * 8192 + off, 16, 1024),
-                                       idS, kk > 0);
+                                for (int kk = 0; kk < D / 16; ++kk) {
+                                    const uint32_t ao = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                                    const uint32_t bo = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
+                                    // S^T = K Q^T ; dP^T = V dO^T  (K-major x K-major)
+                                    mma_ss(tmem + b * 64, dK0 + ao, dst + bo, idS, kk > 0);
+                                    mma_ss(tmem + 128 + b * 64, dV0 + ao, dst + ((C::kTile64 >> 4) + bo), idS,
+                                           kk > 0);
+                                }
+                                mma_commit(smem_u32(&bar_s[b]));
                             }
-                            mma_commit(smem_u32(&bar_s[b]));
+                            __syncwarp();
                             S2TRACE(2, n_glob);
                             if (prev_st >= 0) accumulate(prev_n, prev_st);
                             prev_st = st;
@@ -248,8 +264,11 @@ __global__ void __launch_bounds__(384, 1)
                         }
                     }
                 if (prev_st >= 0) accumulate(prev_n, prev_st);
-                mma_commit(smem_u32(&bar_af));
-                mma_commit(smem_u32(&bar_kve));
+                if (leader) {
+                    mma_commit(smem_u32(&bar_af));
+                    mma_commit(smem_u32(&bar_kve));
+                }
+                __syncwarp();
             }
         }
     } else {
@@ -333,8 +352,10 @@ __global__ void __launch_bounds__(384, 1)
                                 dk[c >> 1] = pack_bf16(dv[0], dv[1]);
                             }
                         }
-                        tmem_st16(tmem + b * 64 + wg * 16 + lane_off, pk);
-                        tmem_st16(tmem + 128 + b * 64 + wg * 16 + lane_off, dk);
+                        // P^T / dS^T of my 32 q columns go into the first half of the
+                        // columns I read (never into the other WG's unread columns)
+                        tmem_st16(tmem + b * 64 + wg * 32 + lane_off, pk);
+                        tmem_st16(tmem + 128 + b * 64 + wg * 32 + lane_off, dk);
                         tmem_st_wait();
                         tc_fence_before();
                         mbar_arrive(smem_u32(&bar_p[b]));
@@ -466,7 +487,7 @@ __global__ void __launch_bounds__(384, 1)
                     const uint32_t base = sSt + st * C::kDqStage;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)  // dQ += dS K  (K chunk as MN-major B)
-                        mma_ts(tmem + 256, tmem + 128 + b * 64 + kk * 8,
+                        mma_ts(tmem + 256, tmem + 128 + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
                                umma_desc_sw128(base + kk * 2048, 8192, 1024), idA,
                                (first && kk == 0) ? 0u : 1u);
                     first = false;
@@ -547,7 +568,7 @@ __global__ void __launch_bounds__(384, 1)
                         dk[c >> 1] = pack_bf16(dv[0], dv[1]);
                     }
                 }
-                tmem_st16(tmem + 128 + b * 64 + wg * 16 + lane_off, dk);
+                tmem_st16(tmem + 128 + b * 64 + wg * 32 + lane_off, dk);  // own columns only
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(smem_u32(&bar_p[b]));

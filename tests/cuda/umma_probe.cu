@@ -376,3 +376,195 @@ extern "C" int probe_dkv_seq(int steps, int variant, long long* host_out) {
     cudaFree(d);
     return e == cudaSuccess ? 0 : 2;
 }
+
+// ---- issue-order probe: 16 MMAs per iteration in a given arrangement --------
+// mode 0: SS N=64, one accumulator, one A region (k-slices cycle)
+// mode 1: SS N=64, two accumulators / two A regions, interleaved (S, dP, S, dP ...)
+// mode 2: SS N=64, two accumulators, grouped (8 x S then 8 x dP)
+// mode 3: SS N=128 interleaved        mode 4: SS N=128 grouped
+// mode 5: TS N=128 two accumulators interleaved (dV, dK)
+// mode 6: SS N=256 interleaved        mode 7: mode 1 with accumulate=0 on each group's first MMA
+// mode 8: mode 2 with accumulate=0 on each group's first MMA
+template <int mode>
+__global__ void __launch_bounds__(128, 1) probe_mix_kernel(int iters, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid / 32;
+    for (int i = tid; i < 131072 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar), 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(smem_u32(&tmem_base_s), 512);
+        tmem_relinquish();
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = tmem_base_s;
+    if (tid == 0) {
+        const uint32_t s0 = smem_u32(smem);
+        const uint32_t sA0 = s0, sA1 = s0 + 32768, sB0 = s0 + 65536, sB1 = s0 + 98304;
+        constexpr int N = (mode == 3 || mode == 4 || mode == 5) ? 128 : (mode == 6 ? 256 : 64);
+        constexpr uint32_t id = umma_idesc_bf16(128, N, 0, mode == 5 ? 1 : 0);
+        const uint32_t acc1 = mode == 6 ? 256 : 128;
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                int which, kk;
+                if (mode == 0) { which = 0; kk = j & 7; }
+                else if (mode == 1 || mode == 3 || mode == 5 || mode == 6 || mode == 7) { which = j & 1; kk = j >> 1; }
+                else { which = j >> 3; kk = j & 7; }
+                const int sub = kk >> 2, off = (kk & 3) * 32;
+                const uint32_t acc = ((mode == 7 || mode == 8) && kk == 0) ? 0u : 1u;
+                if (mode == 5) {
+                    mma_ts(tb + 256 + which * 128 - (which ? 0 : 0), tb + which * 64 + kk * 8,
+                           umma_desc_sw128((which ? sB1 : sB0) + kk * 2048, 8192, 1024), id, acc);
+                } else {
+                    mma_ss(tb + which * acc1, umma_desc_sw128((which ? sA1 : sA0) + sub * 16384 + off, 16, 1024),
+                           umma_desc_sw128((which ? sB1 : sB0) + sub * 16384 + off, 16, 1024), id, acc);
+                }
+            }
+        }
+        const long long t1 = clock64();
+        mma_commit(smem_u32(&bar));
+        mbar_wait(smem_u32(&bar), 0);
+        out[0] = t1 - t0;
+        out[1] = clock64() - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tb, 512);
+}
+
+extern "C" int probe_mix(int mode, int iters, long long* host_out) {
+    long long* d;
+    cudaMalloc(&d, 16);
+    const int smem = 1024 + 131072;
+#define PM(M)                                                                                  \
+    if (mode == M) {                                                                           \
+        cudaFuncSetAttribute(probe_mix_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        probe_mix_kernel<M><<<1, 128, smem>>>(iters, d);                                       \
+    }
+    PM(0) PM(1) PM(2) PM(3) PM(4) PM(5) PM(7) PM(8)
+#undef PM
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(host_out, d, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? 0 : 2;
+}
+
+// ---- the dK/dV step's MMA sequence, unrolled issue, with optional contention --
+// V bit 0: S^T/dP^T (16 x SS N=64)   bit 1: dV/dK (8 x TS N=128)
+// bit 2: warps 4-7 stream TMEM loads of the S/dP columns + P stores (the elementwise WG's traffic)
+// bit 3: warp 2 streams 32 KB TMA bulk loads into a spare smem region
+template <int V>
+__global__ void __launch_bounds__(256, 1) probe_dkv2_kernel(int steps, long long* out, const uint8_t* gsrc) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar, tbar;
+    __shared__ uint32_t tmem_base_s;
+    __shared__ volatile int done;
+    const int tid = threadIdx.x, warp = tid / 32;
+    for (int i = tid; i < 163840 / 4; i += 256) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar), 1);
+        mbar_init(smem_u32(&tbar), 1);
+        fence_mbar_init();
+        done = 0;
+    }
+    if (warp == 0) {
+        tmem_alloc(smem_u32(&tmem_base_s), 512);
+        tmem_relinquish();
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = tmem_base_s;
+    if (tid == 0) {
+        const uint32_t sK = smem_u32(smem), sV = sK + 32768, sQ = sK + 65536, sdO = sQ + 16384;
+        constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0), idA = umma_idesc_bf16(128, 128, 0, 1);
+        const long long t0 = clock64();
+        for (int n = 0; n < steps; ++n) {
+            const int b = n & 1;
+            if (V & 1) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int sub = kk >> 2, off = (kk & 3) * 32;
+                    mma_ss(tb + b * 64, umma_desc_sw128(sK + sub * 16384 + off, 16, 1024),
+                           umma_desc_sw128(sQ + sub * 8192 + off, 16, 1024), idS, kk > 0);
+                    mma_ss(tb + 128 + b * 64, umma_desc_sw128(sV + sub * 16384 + off, 16, 1024),
+                           umma_desc_sw128(sdO + sub * 8192 + off, 16, 1024), idS, kk > 0);
+                }
+            }
+            if (V & 2) {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    mma_ts(tb + 256, tb + b * 64 + kk * 8, umma_desc_sw128(sdO + kk * 2048, 8192, 1024), idA, 1);
+                    mma_ts(tb + 384, tb + 128 + b * 64 + kk * 8, umma_desc_sw128(sQ + kk * 2048, 8192, 1024), idA, 1);
+                }
+            }
+        }
+        mma_commit(smem_u32(&bar));
+        mbar_wait(smem_u32(&bar), 0);
+        out[0] = clock64() - t0;
+        done = 1;
+    }
+    if ((V & 8) && warp == 2 && (tid & 31) == 0) {
+        const uint32_t dst = smem_u32(smem) + 131072;
+        uint32_t ph = 0;
+        for (int it = 0; it < 100000 && !done; ++it) {
+            mbar_expect_tx(smem_u32(&tbar), 32768);
+            for (int c = 0; c < 4; ++c)
+                bulk_load(dst + c * 8192, gsrc + (static_cast<size_t>(it % 64) * 32768) + c * 8192, 8192, smem_u32(&tbar));
+            mbar_wait(smem_u32(&tbar), ph);
+            ph ^= 1;
+        }
+    }
+    if ((V & 4) && warp >= 4) {
+        const uint32_t lo = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        for (int it = 0; it < 400000 && !done; ++it) {
+            uint32_t r[32], d[32];
+            tmem_ld32(tb + lo + (it & 1) * 64, r);
+            tmem_ld32(tb + lo + 128 + (it & 1) * 64, d);
+            tmem_ld_wait();
+            uint32_t w[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) w[j] = r[j] ^ d[j + 16];
+            tmem_st16(tb + lo + 200, w);
+            tmem_st16(tb + lo + 232, w);
+            tmem_st_wait();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tb, 512);
+}
+
+extern "C" int probe_dkv2(int steps, int variant, long long* host_out) {
+    long long* d;
+    cudaMalloc(&d, 16);
+    static uint8_t* gsrc = nullptr;
+    if (!gsrc) {
+        cudaMalloc(&gsrc, 64 * 32768);
+        cudaMemset(gsrc, 0, 64 * 32768);
+    }
+    const int smem = 1024 + 163840;
+#define PD(M)                                                                                         \
+    if (variant == M) {                                                                               \
+        cudaFuncSetAttribute(probe_dkv2_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        probe_dkv2_kernel<M><<<1, 256, smem>>>(steps, d, gsrc);                                       \
+    }
+    PD(1) PD(2) PD(3) PD(7) PD(11) PD(15)
+#undef PD
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(host_out, d, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? 0 : 2;
+}

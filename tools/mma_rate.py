@@ -16,3 +16,15 @@ for kind, name in ((0, "SS"), (1, "TS")):
 for variant, name in ((0, "S,dP + dV,dK"), (1, "S,dP only"), (2, "dV,dK only"), (3, "all + concurrent TMEM loads"), (4, "all + concurrent TMEM ld+st"), (5, "all + concurrent TMA 32KB loads"), (6, "all + 7 ALU-busy warps (issuer = lowest wid)"), (7, "commit after S,dP"), (8, "commit after S,dP and after dV,dK"), (9, "fence::after_thread_sync between groups"), (10, "commit+wait+fence between groups (drain)"), (11, "Q/dO tiles rotate between 2 stages")):
     assert L.probe_dkv_seq(512, variant, out) == 0
     print(f"dkv step sequence [{name}]: {out[0]/512:.0f} cyc/step")
+modes = ["SS64 1acc", "SS64 2acc interleaved", "SS64 2acc grouped", "SS128 interleaved", "SS128 grouped",
+         "TS128 2acc interleaved", "SS256 interleaved", "SS64 interleaved acc0-first", "SS64 grouped acc0-first"]
+for m, name in enumerate(modes):
+    if m == 6:
+        continue
+    assert L.probe_mix(m, 256, out) == 0
+    n = 256 * 16
+    N = 128 if m in (3, 4, 5) else (256 if m == 6 else 64)
+    print(f"mix [{name}]: {out[1]/n:6.1f} cyc/MMA (ideal {N/2:.0f}), issue {out[0]/n:6.1f}")
+for v, name in ((1, "S,dP"), (2, "dV,dK"), (3, "all"), (7, "all + TMEM ld/st"), (11, "all + TMA"), (15, "all + TMEM + TMA")):
+    assert L.probe_dkv2(512, v, out) == 0
+    print(f"dkv2 [{name}]: {out[0]/512:.0f} cyc/step (ideal S,dP 512 + dV,dK 512)")
