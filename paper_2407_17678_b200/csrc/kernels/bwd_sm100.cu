@@ -471,12 +471,18 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
             }
-        } else if (warp == 1 && lane == 0) {
+        } else if (warp == 1) {
+            // whole-warp issuer, elected lane (see the dK/dV kernel)
             constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);
             constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
+            const bool leader = elect_one();
+            const uint64_t dQ0 = umma_desc_sw128(sQ, 16, 1024), ddO0 = umma_desc_sw128(sdO, 16, 1024);
+            const uint64_t dSt0 = umma_desc_sw128(sSt, 16, 1024);
+            const uint64_t dStMN0 = umma_desc_sw128(sSt, 8192, 1024);
             uint32_t it_cnt = 0, st_it = 0, n_glob = 0;
-            for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
-                const FwdItem it = items[i];
+            const int i_end = p.sched[blockIdx.x + 1];
+            for (int i = p.sched[blockIdx.x]; i < i_end; ++i, ++it_cnt) {
+                const int chunk_cnt = warp_uniform(items[i].chunk_cnt);
                 mbar_wait(smem_u32(&bar_qf), it_cnt & 1);
                 bool first = true;
                 auto accumulate = [&](uint32_t n, int st) {
@@ -484,39 +490,45 @@ __global__ void __launch_bounds__(384, 1)
                     mbar_wait(smem_u32(&bar_p[b]), (n >> 1) & 1);
                     if (first && it_cnt > 0) mbar_wait(smem_u32(&bar_ae), (it_cnt - 1) & 1);
                     tc_fence_after();  // A operand (dS) was written to TMEM by tcgen05.st
-                    const uint32_t base = sSt + st * C::kDqStage;
+                    const uint64_t dst = dStMN0 + static_cast<uint64_t>((st * C::kDqStage) >> 4);
+                    if (leader) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)  // dQ += dS K  (K chunk as MN-major B)
-                        mma_ts(tmem + 256, tmem + 128 + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
-                               umma_desc_sw128(base + kk * 2048, 8192, 1024), idA,
-                               (first && kk == 0) ? 0u : 1u);
+                        for (int kk = 0; kk < 4; ++kk)  // dQ += dS K  (K chunk as MN-major B)
+                            mma_ts(tmem + 256, tmem + 128 + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
+                                   dst + ((kk * 2048) >> 4), idA, (first && kk == 0) ? 0u : 1u);
+                        mma_commit(smem_u32(&bar_se[st]));
+                    }
+                    __syncwarp();
                     first = false;
-                    mma_commit(smem_u32(&bar_se[st]));
                 };
                 int prev_st = -1;
                 uint32_t prev_n = 0;
-                for (int n = 0; n < it.chunk_cnt; ++n, ++st_it, ++n_glob) {
+                for (int n = 0; n < chunk_cnt; ++n, ++st_it, ++n_glob) {
                     const int st = st_it % NST;
                     mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
-                    const uint32_t base = sSt + st * C::kDqStage;
+                    const uint64_t dst = dSt0 + static_cast<uint64_t>((st * C::kDqStage) >> 4);
                     const int b = n_glob & 1;
+                    if (leader) {
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const int sub = kk >> 2, off = (kk & 3) * 32;
-                        mma_ss(tmem + b * 64, umma_desc_sw128(sQ + sub * 16384 + off, 16, 1024),
-                               umma_desc_sw128(base + sub * 8192 + off, 16, 1024), idS, kk > 0);
-                        mma_ss(tmem + 128 + b * 64, umma_desc_sw128(sdO + sub * 16384 + off, 16, 1024),
-                               umma_desc_sw128(base + C::kTile64 + sub * 8192 + off, 16, 1024), idS,
-                               kk > 0);
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t ao = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                            const uint32_t bo = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
+                            mma_ss(tmem + b * 64, dQ0 + ao, dst + bo, idS, kk > 0);
+                            mma_ss(tmem + 128 + b * 64, ddO0 + ao, dst + ((C::kTile64 >> 4) + bo), idS, kk > 0);
+                        }
+                        mma_commit(smem_u32(&bar_s[b]));
                     }
-                    mma_commit(smem_u32(&bar_s[b]));
+                    __syncwarp();
                     if (prev_st >= 0) accumulate(prev_n, prev_st);
                     prev_st = st;
                     prev_n = n_glob;
                 }
                 if (prev_st >= 0) accumulate(prev_n, prev_st);
-                mma_commit(smem_u32(&bar_af));
-                mma_commit(smem_u32(&bar_qe));
+                if (leader) {
+                    mma_commit(smem_u32(&bar_af));
+                    mma_commit(smem_u32(&bar_qe));
+                }
+                __syncwarp();
             }
         }
     } else {

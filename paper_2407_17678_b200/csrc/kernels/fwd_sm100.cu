@@ -163,27 +163,40 @@ __global__ void __launch_bounds__(384, 1)
                                              sb * 64, (h ? s.c1 : s.c0) * 64, kvbh, keep);
                 }
             }
-        } else if (warp == 1 && lane == 0) {
+        } else if (warp == 1) {
             // ------------------------------------------------------ MMA issuer
+            // Whole warp on warp-uniform values, one elected lane issues (the
+            // descriptors stay in uniform registers: no per-MMA waterfall).
             constexpr uint32_t idS128 = umma_idesc_bf16(128, 128, 0, 0);
             constexpr uint32_t idS64 = umma_idesc_bf16(128, 64, 0, 0);
             constexpr uint32_t idO = umma_idesc_bf16(128, D, 0, 1);
+            const bool leader = elect_one();
+            const uint64_t dQ0 = umma_desc_sw128(sQ0, 16, 1024);
+            const uint64_t dKV0 = umma_desc_sw128(sKV, 16, 1024);
+            const uint64_t dVmn0 = umma_desc_sw128(sKV + C::kKBytes, 16384, 1024);
             uint32_t kv_it = 0, q_use[2] = {0, 0}, p_cnt[2] = {0, 0}, o_use[2] = {0, 0};
-            for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i) {
-                const PairItem it = p.items[i];
-                const PairStep* steps = p.steps + it.step_off;
-                const bool has[2] = {true, it.has_b != 0};
+            const int i_end = p.sched[blockIdx.x + 1];
+            for (int i = p.sched[blockIdx.x]; i < i_end; ++i) {
+                const int nsteps = warp_uniform(p.items[i].nsteps);
+                const bool has_b = warp_uniform(p.items[i].has_b) != 0;
+                const int64_t step_off = p.items[i].step_off;
+                const PairStep* steps = p.steps + step_off;
+                const bool has[2] = {true, has_b};
                 for (int t = 0; t < 2; ++t)
                     if (has[t]) mbar_wait(smem_u32(&bar_qf[t]), q_use[t] & 1);
                 int pend[2] = {-1, -1};     // step whose P awaits its PV
                 int pend_half[2] = {0, 0};  // 0: both halves, 1: half 0 only, 2: half 1 only
                 bool first_pv[2] = {true, true};
-                for (int n = 0; n <= it.nsteps; ++n) {
-                    PairStep s{};
+                for (int n = 0; n <= nsteps; ++n) {
+                    uint32_t mA0 = 0, mA1 = 0, mB0 = 0, mB1 = 0;
                     uint32_t st = 0;
                     bool k_ready = false;
-                    if (n < it.nsteps) {
-                        s = steps[n];
+                    if (n < nsteps) {
+                        const PairStep sp = steps[n];
+                        mA0 = warp_uniform(sp.a0);
+                        mA1 = warp_uniform(sp.a1);
+                        mB0 = warp_uniform(sp.b0);
+                        mB1 = warp_uniform(sp.b1);
                         st = (kv_it + n) % NST;
                     }
 #pragma unroll
@@ -197,49 +210,68 @@ __global__ void __launch_bounds__(384, 1)
                             if (first_pv[t] && o_use[t] > 0)
                                 mbar_wait(smem_u32(&bar_oe[t]), (o_use[t] - 1) & 1);
                             tc_fence_after();  // P was written to TMEM by tcgen05.st
-                            const uint32_t sV = sKV + sm * C::kStageBytes + C::kKBytes +
-                                                (pend_half[t] == 2 ? 8192u : 0u);
-                            const int nk = pend_half[t] == 0 ? 8 : 4;
-                            for (int kk = 0; kk < nk; ++kk) {
-                                const uint64_t bd = umma_desc_sw128(sV + kk * 2048, 16384, 1024);
-                                mma_ts(tO, tS + kk * 8, bd, idO, (first_pv[t] && kk == 0) ? 0u : 1u);
+                            const uint64_t dv = dVmn0 + static_cast<uint64_t>(
+                                (sm * C::kStageBytes + (pend_half[t] == 2 ? 8192u : 0u)) >> 4);
+                            if (leader) {
+                                if (pend_half[t] == 0) {
+#pragma unroll
+                                    for (int kk = 0; kk < 8; ++kk)
+                                        mma_ts(tO, tS + kk * 8, dv + ((kk * 2048) >> 4), idO,
+                                               (first_pv[t] && kk == 0) ? 0u : 1u);
+                                } else {
+#pragma unroll
+                                    for (int kk = 0; kk < 4; ++kk)
+                                        mma_ts(tO, tS + kk * 8, dv + ((kk * 2048) >> 4), idO,
+                                               (first_pv[t] && kk == 0) ? 0u : 1u);
+                                }
                             }
+                            __syncwarp();
                             first_pv[t] = false;
                             pend[t] = -1;
                         }
-                        if (n < it.nsteps && has[t]) {
-                            const uint32_t m0 = t ? s.b0 : s.a0, m1 = t ? s.b1 : s.a1;
+                        if (n < nsteps && has[t]) {
+                            const uint32_t m0 = t ? mB0 : mA0, m1 = t ? mB1 : mA1;
                             if (m0 | m1) {
                                 if (!k_ready) {
                                     mbar_wait(smem_u32(&bar_kf[st]), ((kv_it + n) / NST) & 1);
                                     k_ready = true;
                                 }
                                 const int half = (m0 && m1) ? 0 : (m0 ? 1 : 2);
-                                const uint32_t sQ = sQ0 + t * C::kQBytes;
-                                const uint32_t sK = sKV + st * C::kStageBytes + (half == 2 ? 8192u : 0u);
+                                const uint64_t dq = dQ0 + static_cast<uint64_t>((t * C::kQBytes) >> 4);
+                                const uint64_t dk = dKV0 + static_cast<uint64_t>(
+                                    (st * C::kStageBytes + (half == 2 ? 8192u : 0u)) >> 4);
+                                if (leader) {
 #pragma unroll
-                                for (int kk = 0; kk < D / 16; ++kk) {
-                                    const int sub = kk >> 2, off = (kk & 3) * 32;
-                                    const uint64_t ad = umma_desc_sw128(sQ + sub * 16384 + off, 16, 1024);
-                                    const uint64_t bd = umma_desc_sw128(sK + sub * 16384 + off, 16, 1024);
-                                    mma_ss(tS, ad, bd, half == 0 ? idS128 : idS64, kk > 0);
+                                    for (int kk = 0; kk < D / 16; ++kk) {
+                                        const uint32_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                                        mma_ss(tS, dq + o, dk + o, half == 0 ? idS128 : idS64, kk > 0);
+                                    }
+                                    mma_commit(smem_u32(&bar_sf[t]));
                                 }
-                                mma_commit(smem_u32(&bar_sf[t]));
+                                __syncwarp();
                                 pend[t] = n;
                                 pend_half[t] = half;
                             }
                         }
                     }
-                    if (n >= 1) mma_commit(smem_u32(&bar_ke[(kv_it + n - 1) % NST]));
+                    if (n >= 1) {
+                        if (leader) mma_commit(smem_u32(&bar_ke[(kv_it + n - 1) % NST]));
+                        __syncwarp();
+                    }
                 }
+                if (leader)
+                    for (int t = 0; t < 2; ++t)
+                        if (has[t]) {
+                            mma_commit(smem_u32(&bar_of[t]));
+                            mma_commit(smem_u32(&bar_qe[t]));
+                        }
+                __syncwarp();
                 for (int t = 0; t < 2; ++t)
                     if (has[t]) {
-                        mma_commit(smem_u32(&bar_of[t]));
-                        mma_commit(smem_u32(&bar_qe[t]));
                         ++o_use[t];
                         ++q_use[t];
                     }
-                kv_it += it.nsteps;
+                kv_it += nsteps;
             }
         }
     } else {
