@@ -240,7 +240,7 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
         for (size_t ui = 0; ui < units.size(); ++ui) {
             const int g = units[ui] % p->num_kv_heads;
             for (const BwdTile& t : L->bwd.tiles)
-                if (t.group == g) bi.push_back({static_cast<int>(ui), t.c0, t.c1, t.count, t.offset});
+                if (t.group == g) bi.push_back({static_cast<int>(ui), t.c0, t.c1, t.count, t.offset, 0, 0});
         }
         // dK/dV cost: 64-row q halves the kernel steps through (a half with
         // no mask bit in either chunk is skipped) for every head of the group.
@@ -254,7 +254,12 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
             }
             halves[t.offset] = h;
         }
-        auto bwd_cost = [&halves, hpg](const s2dev::BwdItem& a) { return halves.at(a.offset) * hpg; };
+        for (auto& it : bi) it.nsteps = static_cast<int32_t>(halves.at(it.offset) * hpg);
+        const size_t nb_all = bi.size();
+        bi.erase(std::remove_if(bi.begin(), bi.end(), [](const s2dev::BwdItem& a) { return a.nsteps == 0; }),
+                 bi.end());
+        w->bwd_dropped = bi.size() != nb_all;
+        auto bwd_cost = [](const s2dev::BwdItem& a) { return int64_t(a.nsteps); };
         const std::vector<int32_t> off_bwd = schedule_items(
             bi, grid, bwd_cost, [](const s2dev::BwdItem& a) { return a.kvbh; }, 4);
         w->num_fwd = static_cast<int>(fi.size());

@@ -92,12 +92,12 @@ struct BwdCfg {
     static constexpr int kDqSmem = 1024 + 2 * kTile128 + kNST * kDqStage;
 };
 
-// Number of (head, entry, half) steps of a dK/dV item: a 64-row half is
-// skipped when neither chunk mask has a bit in its four row groups.
-__device__ __forceinline__ bool half_active(const BwdEntry& e, int half) {
-    return (((e.mask0 | e.mask1) >> (16 * half)) & 0xFFFFu) != 0;
-}
-
+// Stage layout of the dK/dV kernel: Q rows [64][D] | dO rows [64][D] |
+// lse2[64] | delta[64] | meta (4 x u32: first q row, chunk-0 / chunk-1 masks of
+// this 64-row half (row groups 0..3), query data index).  The producer writes
+// meta with a plain shared store before its expect_tx arrive (release), so
+// whoever observes the stage's full barrier sees it: the MMA issuer and the
+// elementwise warps never touch the global entry list.
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     s2_bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(384, 1)
                       const BwdParams p) {
     using C = BwdCfg<D>;
     constexpr int NST = C::kNST;
+    constexpr int kMeta = 2 * C::kTile64 + 512;  // byte offset of a stage's meta
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(384, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sK = smem_u32(smem), sV = sK + C::kTile128;
     const uint32_t sSt = sV + C::kTile128;
+    uint8_t* const gSt = smem + 2 * C::kTile128;  // generic pointer to stage 0
     const BwdItem* items = static_cast<const BwdItem*>(p.items);
     const BwdEntry* ents = static_cast<const BwdEntry*>(p.entries);
 
@@ -140,6 +142,7 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
     // TMEM: S^T[b] at 64b, dP^T[b] at 128+64b, dV at 256, dK at 384.
+    const int i_beg = p.sched[blockIdx.x], i_end = p.sched[blockIdx.x + 1];
 
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(384, 1)
             tma_prefetch(&tmK);
             tma_prefetch(&tmV);
             uint32_t it_cnt = 0, st_it = 0;
-            for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
+            for (int i = i_beg; i < i_end; ++i, ++it_cnt) {
                 const BwdItem it = items[i];
                 if (it_cnt > 0) mbar_wait(smem_u32(&bar_kve), (it_cnt - 1) & 1);
                 const int nc = it.c1 >= 0 ? 2 : 1;
@@ -166,12 +169,16 @@ __global__ void __launch_bounds__(384, 1)
                     for (int e = 0; e < it.count; ++e) {
                         const BwdEntry en = ents[it.offset + e];
                         for (int half = 0; half < 2; ++half) {
-                            if (!half_active(en, half)) continue;
+                            const uint32_t m0 = (en.mask0 >> (16 * half)) & 0xFFFFu;
+                            const uint32_t m1 = (en.mask1 >> (16 * half)) & 0xFFFFu;
+                            if ((m0 | m1) == 0) continue;
                             const int st = st_it % NST;
                             if (st_it >= NST) mbar_wait(smem_u32(&bar_se[st]), ((st_it / NST) + 1) & 1);
                             const uint32_t base = sSt + st * C::kDkvStage;
                             const uint32_t bar = smem_u32(&bar_sf[st]);
                             const int row0 = en.qtile * 128 + half * 64;
+                            *reinterpret_cast<uint4*>(gSt + st * C::kDkvStage + kMeta) =
+                                make_uint4(static_cast<uint32_t>(row0), m0, m1, static_cast<uint32_t>(qbh));
                             mbar_expect_tx(bar, 2 * C::kTile64 + 512);
                             for (int s = 0; s < C::kSub; ++s) {
                                 tma_load_3d(base + s * 8192, &tmQ, bar, s * 64, row0, qbh);
@@ -189,25 +196,20 @@ __global__ void __launch_bounds__(384, 1)
             // ---------------------------------------------------- MMA issuer
             // The whole warp runs the loop on warp-uniform values; one elected
             // lane issues (keeps descriptors in uniform registers: no
-            // per-MMA waterfall loop).
+            // per-MMA waterfall loop).  Per step n: S^T(n), dP^T(n) into TMEM
+            // buffer n&1, then dV, dK += the previous step's P^T, dS^T.
             constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);
             constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
             const bool leader = elect_one();
-            // descriptor of the K / V tiles and of stage 0's Q / dO tiles; SW128
-            // K-major advance along K = +32 B per 16 elements (+2 in the desc)
+            // SW128 K-major advance along K = +32 B per 16 elements (+2 in the desc)
             const uint64_t dK0 = umma_desc_sw128(sK, 16, 1024), dV0 = umma_desc_sw128(sV, 16, 1024);
             const uint64_t dSt0 = umma_desc_sw128(sSt, 16, 1024);
             const uint64_t dStMN0 = umma_desc_sw128(sSt, 8192, 1024);
-            uint32_t it_cnt = 0, st_it = 0, n_glob = 0;
-            const int i_end = p.sched[blockIdx.x + 1];
-            for (int i = p.sched[blockIdx.x]; i < i_end; ++i, ++it_cnt) {
-                const int offset = warp_uniform(static_cast<int>(items[i].offset));
-                const int count = warp_uniform(items[i].count);
+            uint32_t it_cnt = 0, st_it = 0;
+            for (int i = i_beg; i < i_end; ++i, ++it_cnt) {
+                const int nsteps = warp_uniform(items[i].nsteps);
                 mbar_wait(smem_u32(&bar_kvf), it_cnt & 1);
-                bool first = true;
-                int prev_st = -1;
-                uint32_t prev_n = 0;
-                auto accumulate = [&](uint32_t n, int st) {
+                auto accumulate = [&](uint32_t n, int st, bool first) {
                     const int b = n & 1;
                     S2TRACE(3, n);
                     mbar_wait(smem_u32(&bar_p[b]), (n >> 1) & 1);
@@ -219,51 +221,41 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                         for (int kk = 0; kk < ((p.debug & 2) ? 0 : 4); ++kk) {
                             const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-                            // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
                             // K slice kk of P^T / dS^T: WG (kk >> 1) stored it at 32*(kk>>1) + 8*(kk&1)
                             const uint32_t ac = b * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                            // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
                             mma_ts(tmem + 256, tmem + ac, dst + ((C::kTile64 + kk * 2048) >> 4), idA, acc);
                             mma_ts(tmem + 384, tmem + 128 + ac, dst + ((kk * 2048) >> 4), idA, acc);
                         }
                         mma_commit(smem_u32(&bar_se[st]));
                     }
                     __syncwarp();
-                    first = false;
                 };
-                for (int j = 0; j < p.hpg; ++j)
-                    for (int e = 0; e < count; ++e) {
-                        const BwdEntry en = ents[offset + e];
-                        const uint32_t mor = warp_uniform(en.mask0 | en.mask1);
-                        for (int half = 0; half < 2; ++half) {
-                            if (((mor >> (16 * half)) & 0xFFFFu) == 0) continue;
-                            const int st = st_it % NST;
-                            S2TRACE(0, n_glob);
-                            mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
-                            S2TRACE(1, n_glob);
-                            const uint64_t dst = dSt0 + static_cast<uint64_t>((st * C::kDkvStage) >> 4);
-                            const int b = n_glob & 1;
-                            if (leader) {
+                for (int s = 0; s < nsteps; ++s) {
+                    const uint32_t n = st_it;
+                    const int st = st_it % NST;
+                    S2TRACE(0, n);
+                    mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
+                    S2TRACE(1, n);
+                    const uint64_t dst = dSt0 + static_cast<uint64_t>((st * C::kDkvStage) >> 4);
+                    const int b = n & 1;
+                    if (leader) {
 #pragma unroll
-                                for (int kk = 0; kk < D / 16; ++kk) {
-                                    const uint32_t ao = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-                                    const uint32_t bo = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
-                                    // S^T = K Q^T ; dP^T = V dO^T  (K-major x K-major)
-                                    mma_ss(tmem + b * 64, dK0 + ao, dst + bo, idS, kk > 0);
-                                    mma_ss(tmem + 128 + b * 64, dV0 + ao, dst + ((C::kTile64 >> 4) + bo), idS,
-                                           kk > 0);
-                                }
-                                mma_commit(smem_u32(&bar_s[b]));
-                            }
-                            __syncwarp();
-                            S2TRACE(2, n_glob);
-                            if (prev_st >= 0) accumulate(prev_n, prev_st);
-                            prev_st = st;
-                            prev_n = n_glob;
-                            ++n_glob;
-                            ++st_it;
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t ao = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                            const uint32_t bo = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
+                            // S^T = K Q^T ; dP^T = V dO^T  (K-major x K-major)
+                            mma_ss(tmem + b * 64, dK0 + ao, dst + bo, idS, kk > 0);
+                            mma_ss(tmem + 128 + b * 64, dV0 + ao, dst + ((C::kTile64 >> 4) + bo), idS, kk > 0);
                         }
+                        mma_commit(smem_u32(&bar_s[b]));
                     }
-                if (prev_st >= 0) accumulate(prev_n, prev_st);
+                    __syncwarp();
+                    S2TRACE(2, n);
+                    if (s > 0) accumulate(n - 1, (st_it - 1) % NST, s == 1);
+                    ++st_it;
+                }
+                accumulate(st_it - 1, (st_it - 1) % NST, nsteps == 1);
                 if (leader) {
                     mma_commit(smem_u32(&bar_af));
                     mma_commit(smem_u32(&bar_kve));
@@ -278,92 +270,85 @@ __global__ void __launch_bounds__(384, 1)
         const int kr = tid & 127;         // key row == TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const float sl2 = p.scale_log2;
-        uint32_t it_cnt = 0, st_it = 0, n_glob = 0;
-        for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
+        const int cg = (kr & 63) >> 4;
+        const int hk = kr >> 6;
+        uint32_t it_cnt = 0, st_it = 0;
+        for (int i = i_beg; i < i_end; ++i, ++it_cnt) {
             const BwdItem it = items[i];
-            const int hk = kr >> 6;
             const int chunk = hk ? it.c1 : it.c0;
-            const int cg = (kr & 63) >> 4;
             const int key_pos = chunk * 64 + (kr & 63);
             const bool key_ok = chunk >= 0 && key_pos < p.N;
-            for (int j = 0; j < p.hpg; ++j)
-                for (int e = 0; e < it.count; ++e) {
-                    const BwdEntry en = ents[it.offset + e];
-                    for (int half = 0; half < 2; ++half) {
-                        if (!half_active(en, half)) continue;
-                        const int st = st_it % NST;
-                        const int b = n_glob & 1;
-                        if (tid == 128) S2TRACE(5, n_glob);
-                        mbar_wait(smem_u32(&bar_s[b]), (n_glob >> 1) & 1);
-                        if (tid == 128) S2TRACE(6, n_glob);
-                        tc_fence_after();
-                        if (p.debug & 1) {
-                            tc_fence_before();
-                            mbar_arrive(smem_u32(&bar_p[b]));
-                            ++n_glob;
-                            ++st_it;
-                            continue;
+            for (int s = 0; s < it.nsteps; ++s, ++st_it) {
+                const int st = st_it % NST;
+                const int b = st_it & 1;
+                if (tid == 128) S2TRACE(5, st_it);
+                mbar_wait(smem_u32(&bar_s[b]), (st_it >> 1) & 1);
+                if (tid == 128) S2TRACE(6, st_it);
+                tc_fence_after();
+                if (p.debug & 1) {
+                    tc_fence_before();
+                    mbar_arrive(smem_u32(&bar_p[b]));
+                    continue;
+                }
+                uint32_t su[32], du[32];
+                tmem_ld32(tmem + b * 64 + wg * 32 + lane_off, su);
+                tmem_ld32(tmem + 128 + b * 64 + wg * 32 + lane_off, du);
+                // lse2 / delta / meta of this stage: shared-space vector loads
+                // (broadcast).  They were written by a bulk copy / the producer:
+                // observe the stage barrier ourselves (already complete; the
+                // stage cannot be refilled before our P arrives).
+                mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
+                const uint32_t sbase = sSt + st * C::kDkvStage;
+                const uint4 meta = *reinterpret_cast<const uint4*>(gSt + st * C::kDkvStage + kMeta);
+                const uint32_t m = key_ok ? (hk ? meta.z : meta.y) : 0u;
+                const uint32_t sl = sbase + 2 * C::kTile64 + wg * 128;
+                const bool on0 = (m >> (wg * 8 + cg)) & 1u;
+                const bool on1 = (m >> (wg * 8 + 4 + cg)) & 1u;
+                const int q0 = static_cast<int>(meta.x) + wg * 32;
+                float l2v[32], dlv[32];
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    const float4 a = lds_f4(sl + c * 4), d4 = lds_f4(sl + 256 + c * 4);
+                    l2v[c] = a.x; l2v[c + 1] = a.y; l2v[c + 2] = a.z; l2v[c + 3] = a.w;
+                    dlv[c] = d4.x; dlv[c + 1] = d4.y; dlv[c + 2] = d4.z; dlv[c + 3] = d4.w;
+                }
+                tmem_ld_wait();
+                uint32_t pk[16], dk[16];
+                if (on0 && on1 && key_pos <= q0) {
+                    // fully attended 32 columns, no causal cut: no per-element masking
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        const float p0 = fast_exp2(fmaf(__uint_as_float(su[c]), sl2, -l2v[c]));
+                        const float p1 = fast_exp2(fmaf(__uint_as_float(su[c + 1]), sl2, -l2v[c + 1]));
+                        pk[c >> 1] = pack_bf16(p0, p1);
+                        dk[c >> 1] = pack_bf16(p0 * (__uint_as_float(du[c]) - dlv[c]),
+                                               p1 * (__uint_as_float(du[c + 1]) - dlv[c + 1]));
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        float pv[2], dv[2];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int cc = c + u;
+                            const bool ok = (cc < 16 ? on0 : on1) && key_pos <= q0 + cc;
+                            const float pe = fast_exp2(fmaf(__uint_as_float(su[cc]), sl2, -l2v[cc]));
+                            pv[u] = ok ? pe : 0.f;
+                            dv[u] = ok ? pe * (__uint_as_float(du[cc]) - dlv[cc]) : 0.f;
                         }
-                        uint32_t su[32], du[32];
-                        tmem_ld32(tmem + b * 64 + wg * 32 + lane_off, su);
-                        tmem_ld32(tmem + 128 + b * 64 + wg * 32 + lane_off, du);
-                        const uint32_t m = key_ok ? (hk ? en.mask1 : en.mask0) : 0u;
-                        // lse2 / delta of my 32 q columns: shared-space vector loads (broadcast).
-                        // They were written by a bulk copy: observe its barrier ourselves
-                        // (already complete; the stage cannot be refilled before our P).
-                        mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
-                        const uint32_t sl = sSt + st * C::kDkvStage + 2 * C::kTile64 + wg * 128;
-                        const int g0 = half * 4 + wg * 2;  // q row groups of my 32 columns
-                        const bool on0 = (m >> (g0 * 4 + cg)) & 1u;
-                        const bool on1 = (m >> ((g0 + 1) * 4 + cg)) & 1u;
-                        const int q0 = en.qtile * 128 + half * 64 + wg * 32;
-                        float l2v[32], dlv[32];
-#pragma unroll
-                        for (int c = 0; c < 32; c += 4) {
-                            const float4 a = lds_f4(sl + c * 4), d4 = lds_f4(sl + 256 + c * 4);
-                            l2v[c] = a.x; l2v[c + 1] = a.y; l2v[c + 2] = a.z; l2v[c + 3] = a.w;
-                            dlv[c] = d4.x; dlv[c + 1] = d4.y; dlv[c + 2] = d4.z; dlv[c + 3] = d4.w;
-                        }
-                        tmem_ld_wait();
-                        uint32_t pk[16], dk[16];
-                        if (on0 && on1 && key_pos <= q0) {
-                            // fully attended 32 columns, no causal cut: no per-element masking
-#pragma unroll
-                            for (int c = 0; c < 32; c += 2) {
-                                const float p0 = fast_exp2(fmaf(__uint_as_float(su[c]), sl2, -l2v[c]));
-                                const float p1 = fast_exp2(fmaf(__uint_as_float(su[c + 1]), sl2, -l2v[c + 1]));
-                                pk[c >> 1] = pack_bf16(p0, p1);
-                                dk[c >> 1] = pack_bf16(p0 * (__uint_as_float(du[c]) - dlv[c]),
-                                                       p1 * (__uint_as_float(du[c + 1]) - dlv[c + 1]));
-                            }
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < 32; c += 2) {
-                                float pv[2], dv[2];
-#pragma unroll
-                                for (int u = 0; u < 2; ++u) {
-                                    const int cc = c + u;
-                                    const bool ok = (cc < 16 ? on0 : on1) && key_pos <= q0 + cc;
-                                    const float pe = fast_exp2(fmaf(__uint_as_float(su[cc]), sl2, -l2v[cc]));
-                                    pv[u] = ok ? pe : 0.f;
-                                    dv[u] = ok ? pe * (__uint_as_float(du[cc]) - dlv[cc]) : 0.f;
-                                }
-                                pk[c >> 1] = pack_bf16(pv[0], pv[1]);
-                                dk[c >> 1] = pack_bf16(dv[0], dv[1]);
-                            }
-                        }
-                        // P^T / dS^T of my 32 q columns go into the first half of the
-                        // columns I read (never into the other WG's unread columns)
-                        tmem_st16(tmem + b * 64 + wg * 32 + lane_off, pk);
-                        tmem_st16(tmem + 128 + b * 64 + wg * 32 + lane_off, dk);
-                        tmem_st_wait();
-                        tc_fence_before();
-                        mbar_arrive(smem_u32(&bar_p[b]));
-                        if (tid == 128) S2TRACE(7, n_glob);
-                        ++n_glob;
-                        ++st_it;
+                        pk[c >> 1] = pack_bf16(pv[0], pv[1]);
+                        dk[c >> 1] = pack_bf16(dv[0], dv[1]);
                     }
                 }
+                // P^T / dS^T of my 32 q columns go into the first half of the
+                // columns I read (never into the other WG's unread columns)
+                tmem_st16(tmem + b * 64 + wg * 32 + lane_off, pk);
+                tmem_st16(tmem + 128 + b * 64 + wg * 32 + lane_off, dk);
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(smem_u32(&bar_p[b]));
+                if (tid == 128) S2TRACE(7, st_it);
+            }
             // ---------------------------------------------------- epilogue
             mbar_wait(smem_u32(&bar_af), it_cnt & 1);
             tc_fence_after();

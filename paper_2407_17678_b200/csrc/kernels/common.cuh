@@ -20,6 +20,8 @@ struct BwdItem {
     int32_t c0, c1;  // chunks (c1 = -1 when single)
     int32_t count;   // q tiles visited
     int64_t offset;  // into the BwdEntry array
+    int32_t nsteps;  // (query head, q tile, active 64-row half) steps = hpg * active halves
+    int32_t pad;
 };
 struct BwdEntry {
     int32_t qtile;

@@ -44,6 +44,7 @@ struct WorkItems {
     int num_pair = 0;
     DevBuf bwd;       // s2dev::BwdItem[]
     int num_bwd = 0;
+    bool bwd_dropped = false;  // key tiles nobody attends (user CSR without diagonal): dK/dV = 0
     DevBuf fwd_sched, pair_sched, bwd_sched;  // int[grid + 1] per-CTA item ranges
     int grid = 0;
     DevBuf simt_bh;   // int[num_bh] data index
