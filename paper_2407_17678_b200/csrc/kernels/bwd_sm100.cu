@@ -249,6 +249,10 @@ __global__ void __launch_bounds__(384, 1)
                             mma_ss(tmem + 128 + b * 64, dV0 + ao, dst + ((C::kTile64 >> 4) + bo), idS, kk > 0);
                         }
                         mma_commit(smem_u32(&bar_s[b]));
+                        // K / V are read by the S^T / dP^T MMAs only: release them after
+                        // the item's last ones so the next item's K / V load overlaps the
+                        // last dV / dK update and the epilogue.
+                        if (s == nsteps - 1) mma_commit(smem_u32(&bar_kve));
                     }
                     __syncwarp();
                     S2TRACE(2, n);
@@ -256,10 +260,7 @@ __global__ void __launch_bounds__(384, 1)
                     ++st_it;
                 }
                 accumulate(st_it - 1, (st_it - 1) % NST, nsteps == 1);
-                if (leader) {
-                    mma_commit(smem_u32(&bar_af));
-                    mma_commit(smem_u32(&bar_kve));
-                }
+                if (leader) mma_commit(smem_u32(&bar_af));
                 __syncwarp();
             }
         }
