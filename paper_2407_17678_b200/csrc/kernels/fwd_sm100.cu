@@ -301,18 +301,18 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_after();
                 float sv[128];
                 {
-                    uint32_t u[32];
+                    // all column chunks in flight, one wait
+                    uint32_t* u = reinterpret_cast<uint32_t*>(sv);
+                    tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(u));
+                    tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+                    if (both) {
+                        tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(u + 64));
+                        tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(u + 96));
+                    }
+                    tmem_ld_wait();
+                    if (!both) {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        if (c < 2 || both) {
-                            tmem_ld32(tS + c * 32, u);
-                            tmem_ld_wait();
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) sv[c * 32 + j] = __uint_as_float(u[j]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) sv[c * 32 + j] = -INFINITY;
-                        }
+                        for (int j = 64; j < 128; ++j) sv[j] = -INFINITY;
                     }
                 }
                 if (both) {
@@ -352,20 +352,38 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 m_run = m_use;
                 const float base = (m_use == -INFINITY) ? 0.f : m_use;
-                float sum = 0.f;
+                // P = 2^(S*scale*log2e - m): packed FFMA2, 3/4 of the pairs on MUFU.EX2 and
+                // 1/4 on the FMA pipe (exp2_poly2) so the XU pipe stops pacing the tile
+                const uint64_t sl2v = f2_pack(sl2, sl2), nbase = f2_pack(-base, -base);
+                uint64_t acc = f2_pack(0.f, 0.f);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     if (c < 2 || both) {
                         uint32_t pk[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            const float p0 = fast_exp2(fmaf(sv[c * 32 + 2 * j], sl2, -base));
-                            const float p1 = fast_exp2(fmaf(sv[c * 32 + 2 * j + 1], sl2, -base));
-                            sum += p0 + p1;
+                            const uint64_t x = ffma2(f2_pack(sv[c * 32 + 2 * j], sv[c * 32 + 2 * j + 1]), sl2v, nbase);
+                            uint64_t pr;
+                            if ((j & 3) == 3) {
+                                pr = exp2_poly2(x);
+                            } else {
+                                float x0, x1;
+                                f2_unpack(x, x0, x1);
+                                pr = f2_pack(fast_exp2(x0), fast_exp2(x1));
+                            }
+                            acc = fadd2(acc, pr);
+                            float p0, p1;
+                            f2_unpack(pr, p0, p1);
                             pk[j] = pack_bf16(p0, p1);
                         }
                         tmem_st16(tS + c * 16, pk);
                     }
+                }
+                float sum;
+                {
+                    float a0, a1;
+                    f2_unpack(acc, a0, a1);
+                    sum = a0 + a1;
                 }
                 l_run += sum;
                 tmem_st_wait();

@@ -219,6 +219,53 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two lanes' worth per slot).
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+    uint64_t d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+    return d;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t d, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(d));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// 2^x for a pair on the FMA pipe (offloads MUFU.EX2): x clamped to >= -127
+// (-inf -> exactly +0), round-to-nearest split x = j + f, f in [-1/2, 1/2],
+// 2^f by a cubic with c0 = 1 (max rel. error 3e-4, below bf16 rounding of
+// P), exponent added as an integer.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+    float x0, x1;
+    f2_unpack(x, x0, x1);
+    x = f2_pack(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+    const uint64_t magic = f2_pack(12582912.f, 12582912.f);  // 1.5 * 2^23
+    const uint64_t t = fadd2(x, magic);
+    const uint64_t r = fadd2(t, f2_pack(-12582912.f, -12582912.f));
+    uint64_t f;
+    {
+        float r0, r1, y0, y1;
+        f2_unpack(r, r0, r1);
+        f2_unpack(x, y0, y1);
+        f = fadd2(x, f2_pack(-r0, -r1));
+    }
+    uint64_t pp = ffma2(f2_pack(0.05295114f, 0.05295114f), f, f2_pack(0.24165067f, 0.24165067f));
+    pp = ffma2(pp, f, f2_pack(0.6935366f, 0.6935366f));
+    pp = ffma2(pp, f, f2_pack(1.0f, 1.0f));
+    float p0, p1, t0, t1;
+    f2_unpack(pp, p0, p1);
+    f2_unpack(t, t0, t1);
+    return f2_pack(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+                   __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
+
 __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
