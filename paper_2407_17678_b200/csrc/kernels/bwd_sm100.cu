@@ -613,6 +613,7 @@ static int g_debug = 0;
 extern "C" void s2_debug_set_mode(int m) { g_debug = m; }
 // Debug hook (not in s2attn.h): a device buffer of 8 x 2048 int64 for CTA-0 step timestamps.
 extern "C" void s2_debug_set_trace(void* dev_buf) { g_trace = static_cast<long long*>(dev_buf); }
+long long* s2_debug_trace_buffer() { return g_trace; }
 
 cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* dout,
                                const float* lse, float* delta, float* lse2, int num_bh, int N,

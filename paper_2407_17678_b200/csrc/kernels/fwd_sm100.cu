@@ -49,7 +49,14 @@ struct Fwd2Params {
     int seq_len;
     int hpg;
     float scale_log2;
+    long long* trace;  // debug: per-step clock64 of CTA 0 (nullptr = off)
 };
+
+#define S2FTRACE(slot, n)                                                      \
+    do {                                                                       \
+        if (p.trace && blockIdx.x == 0 && (n) < 2048)                          \
+            p.trace[(slot) * 2048 + (n)] = clock64();                          \
+    } while (0)
 
 template <int D>
 struct Fwd2Cfg {
@@ -187,12 +194,14 @@ __global__ void __launch_bounds__(384, 1)
                 int pend[2] = {-1, -1};     // step whose P awaits its PV
                 int pend_half[2] = {0, 0};  // 0: both halves, 1: half 0 only, 2: half 1 only
                 bool first_pv[2] = {true, true};
+                PairStep nxt = steps[0];  // software-pipelined step descriptor
                 for (int n = 0; n <= nsteps; ++n) {
                     uint32_t mA0 = 0, mA1 = 0, mB0 = 0, mB1 = 0;
                     uint32_t st = 0;
                     bool k_ready = false;
                     if (n < nsteps) {
-                        const PairStep sp = steps[n];
+                        const PairStep sp = nxt;
+                        if (n + 1 < nsteps) nxt = steps[n + 1];
                         mA0 = warp_uniform(sp.a0);
                         mA1 = warp_uniform(sp.a1);
                         mB0 = warp_uniform(sp.b0);
@@ -205,7 +214,9 @@ __global__ void __launch_bounds__(384, 1)
                         if (pend[t] >= 0) {
                             const uint32_t sm = (kv_it + pend[t]) % NST;
                             mbar_wait(smem_u32(&bar_vf[sm]), ((kv_it + pend[t]) / NST) & 1);
+                            if (t == 0 && lane == 0) S2FTRACE(0, p_cnt[0]);
                             mbar_wait(smem_u32(&bar_pf[t]), p_cnt[t] & 1);
+                            if (t == 0 && lane == 0) S2FTRACE(1, p_cnt[0]);
                             ++p_cnt[t];
                             if (first_pv[t] && o_use[t] > 0)
                                 mbar_wait(smem_u32(&bar_oe[t]), (o_use[t] - 1) & 1);
@@ -233,7 +244,9 @@ __global__ void __launch_bounds__(384, 1)
                             const uint32_t m0 = t ? mB0 : mA0, m1 = t ? mB1 : mA1;
                             if (m0 | m1) {
                                 if (!k_ready) {
+                                    if (lane == 0) S2FTRACE(2, kv_it + n);
                                     mbar_wait(smem_u32(&bar_kf[st]), ((kv_it + n) / NST) & 1);
+                                    if (lane == 0) S2FTRACE(3, kv_it + n);
                                     k_ready = true;
                                 }
                                 const int half = (m0 && m1) ? 0 : (m0 ? 1 : 2);
@@ -291,12 +304,16 @@ __global__ void __launch_bounds__(384, 1)
             const int row0 = (2 * it.qpair + t) * 128;
             const int q_pos = row0 + r;
             float m_run = -INFINITY, l_run = 0.f;
+            PairStep nxt = steps[0];  // software-pipelined: step n+1 loads during step n
             for (int n = 0; n < it.nsteps; ++n) {
-                const PairStep s = steps[n];
+                const PairStep s = nxt;
+                if (n + 1 < it.nsteps) nxt = steps[n + 1];
                 const uint32_t m0 = t ? s.b0 : s.a0, m1 = t ? s.b1 : s.a1;
                 if (!(m0 | m1)) continue;
                 const bool both = m0 && m1;
+                if (r == 0) S2FTRACE(4 + 2 * t, s_cnt);
                 mbar_wait(smem_u32(&bar_sf[t]), s_cnt & 1);
+                if (r == 0) S2FTRACE(5 + 2 * t, s_cnt);
                 ++s_cnt;
                 tc_fence_after();
                 float sv[128];
@@ -321,9 +338,16 @@ __global__ void __launch_bounds__(384, 1)
                 } else {
                     apply_mask(sv, m0 ? s.c0 : s.c1, m0 ? m0 : m1, rg, q_pos, row0);
                 }
-                float mx = sv[0];
+                // row max: 8 independent chains (a single chain is ~64 dependent FMNMX3)
+                float mxa[8];
 #pragma unroll
-                for (int j = 1; j < 128; ++j) mx = fmaxf(mx, sv[j]);
+                for (int k = 0; k < 8; ++k) mxa[k] = fmaxf(sv[k], sv[k + 8]);
+#pragma unroll
+                for (int j = 16; j < 128; j += 16)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) mxa[k] = fmaxf(mxa[k], fmaxf(sv[j + k], sv[j + k + 8]));
+                const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                                       fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
                 const float m_tile = mx * sl2;
                 float m_use = m_run;
                 bool rescale = false;
@@ -355,7 +379,7 @@ __global__ void __launch_bounds__(384, 1)
                 // P = 2^(S*scale*log2e - m): packed FFMA2, 3/4 of the pairs on MUFU.EX2 and
                 // 1/4 on the FMA pipe (exp2_poly2) so the XU pipe stops pacing the tile
                 const uint64_t sl2v = f2_pack(sl2, sl2), nbase = f2_pack(-base, -base);
-                uint64_t acc = f2_pack(0.f, 0.f);
+                uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};  // +0.0f pairs; 4 independent chains
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     if (c < 2 || both) {
@@ -371,7 +395,7 @@ __global__ void __launch_bounds__(384, 1)
                                 f2_unpack(x, x0, x1);
                                 pr = f2_pack(fast_exp2(x0), fast_exp2(x1));
                             }
-                            acc = fadd2(acc, pr);
+                            acc[j & 3] = fadd2(acc[j & 3], pr);
                             float p0, p1;
                             f2_unpack(pr, p0, p1);
                             pk[j] = pack_bf16(p0, p1);
@@ -382,7 +406,7 @@ __global__ void __launch_bounds__(384, 1)
                 float sum;
                 {
                     float a0, a1;
-                    f2_unpack(acc, a0, a1);
+                    f2_unpack(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), a0, a1);
                     sum = a0 + a1;
                 }
                 l_run += sum;
@@ -443,6 +467,7 @@ static cudaError_t launch(const CUtensorMap& q, const CUtensorMap& k, const CUte
 }  // namespace s2dev
 
 // Host entry used by capi.cpp: items grouped per CTA, sched = [grid + 1] offsets.
+long long* s2_debug_trace_buffer();
 cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtensorMap& k,
                                 const CUtensorMap& v, const void* items, const int* sched,
                                 int grid, const void* steps, __nv_bfloat16* out, float* lse,
@@ -450,7 +475,7 @@ cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtens
     if (grid == 0) return cudaSuccess;
     s2dev::Fwd2Params p{static_cast<const s2dev::PairItem*>(items), sched,
                         static_cast<const s2dev::PairStep*>(steps), out, lse, seq_len, hpg,
-                        scale_log2};
+                        scale_log2, s2_debug_trace_buffer()};
     if (head_dim == 128) return s2dev::launch<128>(q, k, v, p, grid, stream);
     if (head_dim == 64) return s2dev::launch<64>(q, k, v, p, grid, stream);
     return cudaErrorInvalidValue;

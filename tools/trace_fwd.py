@@ -1,0 +1,31 @@
+"""Debug: CTA-0 per-step timeline of the forward kernel (s2_debug_set_trace)."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2407_17678_b200 as s2
+
+L = s2.lib()
+L.s2_debug_set_trace.argtypes = [ctypes.c_void_p]
+plan = s2.Plan.from_config(s2.make_s2_config(32768, 32, local_blocks=4, vert_stride=16))
+mk = lambda: torch.randn(1, 32, 32768, 128, device="cuda", dtype=torch.bfloat16)  # noqa
+q, k, v = mk(), mk(), mk()
+out, lse = s2.s2_attn_fwd(plan, q, k, v)
+tr = torch.zeros(8 * 2048, dtype=torch.int64, device="cuda")
+L.s2_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
+s2.s2_attn_fwd(plan, q, k, v, out=out, lse=lse)
+torch.cuda.synchronize()
+L.s2_debug_set_trace(None)
+t = tr.cpu().numpy().reshape(8, 2048).astype(np.int64)
+n = int((t[5] > 0).sum())
+m = lambda a: float(np.median(a))  # noqa
+lo, hi = 20, min(n, 1500)
+print("tile-0 softmax steps traced", n)
+print("softmax0: wait S", m(t[5, lo:hi] - t[4, lo:hi]), " step period", m(np.diff(t[5, lo:hi])))
+print("softmax0: S ok -> next wait (compute+store+arrive)", m(t[4, lo + 1:hi + 1] - t[5, lo:hi]))
+print("softmax1: wait S", m(t[7, lo:hi] - t[6, lo:hi]), " compute", m(t[6, lo + 1:hi + 1] - t[7, lo:hi]))
+print("MMA: wait P0", m(t[1, lo:hi] - t[0, lo:hi]), " wait K", m(t[3, lo:hi] - t[2, lo:hi]))
