@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -130,12 +131,17 @@ Lists* get_lists(s2_plan* p, int seq_len, int* status) {
 // items regrouped per CTA plus offsets [grid + 1].
 template <class T, class Cost, class Key>
 static std::vector<int32_t> schedule_items(std::vector<T>& items, int grid, Cost cost, Key key,
-                                           int64_t overhead) {
+                                           int64_t overhead, int key_group = 0) {
     auto cls = [&](const T& a) {
         const double c = static_cast<double>(cost(a) + overhead);
         return static_cast<int>(std::floor(4.0 * std::log2(std::max(1.0, c))));
     };
+    // key_group > 0: keys (heads) are swept in groups of key_group, LPT inside a group
+    // (bounds the L2 working set of streamed operands to a group's heads)
+    auto grp = [&](const T& a) { return key_group > 0 ? static_cast<int64_t>(key(a)) / key_group : 0; };
     std::stable_sort(items.begin(), items.end(), [&](const T& a, const T& b) {
+        const auto ga = grp(a), gb = grp(b);
+        if (ga != gb) return ga < gb;
         const int ca = cls(a), cb = cls(b);
         if (ca != cb) return ca > cb;
         const auto ka = key(a), kb = key(b);
@@ -160,6 +166,11 @@ static std::vector<int32_t> schedule_items(std::vector<T>& items, int grid, Cost
         off[c + 1] = static_cast<int32_t>(items.size());
     }
     return off;
+}
+
+static int dkv_group() {
+    const char* e = getenv("S2_DKV_GROUP");
+    return e ? atoi(e) : 0;
 }
 
 // Units are (batch, kv-group); local data index of query head j of the
@@ -261,7 +272,7 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
         w->bwd_dropped = bi.size() != nb_all;
         auto bwd_cost = [](const s2dev::BwdItem& a) { return int64_t(a.nsteps); };
         const std::vector<int32_t> off_bwd = schedule_items(
-            bi, grid, bwd_cost, [](const s2dev::BwdItem& a) { return a.kvbh; }, 4);
+            bi, grid, bwd_cost, [](const s2dev::BwdItem& a) { return a.kvbh; }, 4, dkv_group());
         w->num_fwd = static_cast<int>(fi.size());
         w->num_bwd = static_cast<int>(bi.size());
         w->grid = grid;

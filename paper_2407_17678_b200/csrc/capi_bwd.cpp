@@ -8,11 +8,10 @@ cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* do
                                const float* lse, float* delta, float* lse2, int num_bh, int N,
                                int Npad, int D, cudaStream_t stream);
 cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CUtensorMap& dout,
-                                const CUtensorMap& k, const CUtensorMap& v, const void* items,
-                                const int* sched, int grid, const void* entries,
-                                const float* lse2, const float* delta, __nv_bfloat16* g0,
-                                __nv_bfloat16* g1, int N, int Npad, int hpg, float scale,
-                                cudaStream_t stream);
+                                const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o0,
+                                const CUtensorMap& o1, const void* items, const int* sched, int grid,
+                                const void* entries, const float* lse2, const float* delta,
+                                int N, int Npad, int hpg, float scale, cudaStream_t stream);
 
 using namespace s2;
 
@@ -88,20 +87,18 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
                 (e = cudaMemsetAsync(a->dv, 0, bytes, st)) != cudaSuccess)
                 return cuda_fail(e, "s2_attn_bwd memset");
         }
+        const CUtensorMap mdk = make_map_bf16_3d(a->dk, D, N, nkv, 64, 64);
+        const CUtensorMap mdv = make_map_bf16_3d(a->dv, D, N, nkv, 64, 64);
+        const CUtensorMap mdq = make_map_bf16_3d(a->dq, D, N, nqbh, 64, 128);
         {
             ProfScope prof("bwd_dkv_sm100", st);
-            e = s2_launch_bwd_sm100(0, D, q64, do64, mk, mv, w->bwd.ptr, w->bwd_sched.as<int>(),
-                                    w->grid, L->d_entries.ptr, lse2, delta,
-                                    static_cast<__nv_bfloat16*>(a->dk),
-                                    static_cast<__nv_bfloat16*>(a->dv), N, Npad, hpg,
-                                    float(scale), st);
+            e = s2_launch_bwd_sm100(0, D, q64, do64, mk, mv, mdk, mdv, w->bwd.ptr, w->bwd_sched.as<int>(),
+                                    w->grid, L->d_entries.ptr, lse2, delta, N, Npad, hpg, float(scale), st);
         }
         if (e == cudaSuccess) {
             ProfScope prof("bwd_dq_sm100", st);
-            e = s2_launch_bwd_sm100(1, D, q128, do128, mk, mv, w->fwd.ptr, w->fwd_sched.as<int>(),
-                                    w->grid, L->d_chunks.ptr, lse2, delta,
-                                    static_cast<__nv_bfloat16*>(a->dq), nullptr, N, Npad, hpg,
-                                    float(scale), st);
+            e = s2_launch_bwd_sm100(1, D, q128, do128, mk, mv, mdq, mdq, w->fwd.ptr, w->fwd_sched.as<int>(),
+                                    w->grid, L->d_chunks.ptr, lse2, delta, N, Npad, hpg, float(scale), st);
         }
     } catch (const std::exception& ex) {
         return fail(S2_ERR_CUDA, ex.what());

@@ -73,7 +73,7 @@ struct BwdParams {
 
 #define S2TRACE(slot, n)                                                       \
     do {                                                                       \
-        if (p.trace && blockIdx.x == 0 && (n) < 2048)                          \
+        if (p.trace && blockIdx.x == 0 && (n) < 2048)  /* 16 slots x 2048 */   \
             p.trace[(slot) * 2048 + (n)] = clock64();                          \
     } while (0)
 
@@ -82,14 +82,17 @@ struct BwdCfg {
     static constexpr int kSub = D / 64;
     static constexpr int kTile128 = kSub * 16384;  // 128 rows x D bf16
     static constexpr int kTile64 = kSub * 8192;    // 64 rows x D bf16
-    static constexpr int kNST = 4;
-    // dkv: resident K, V (128 keys); stages: Q64, dO64, lse2[64], delta[64]
-    // lse/delta (512 B) padded so every stage stays 1024-B aligned (SW128 atoms).
-    static constexpr int kDkvStage = 2 * kTile64 + 1024;
-    static constexpr int kDkvSmem = 1024 + 2 * kTile128 + kNST * kDkvStage;
-    // dq: resident Q, dO (128 rows); stages: K64, V64
+    // dkv: resident K, V (128 keys); kNSTkv stages of Q64, dO64 (1024-B aligned
+    // SW128 tiles); an aux slot per stage (lse2[64], delta[64], meta); the
+    // epilogue's staging tiles for the TMA stores of dV and dK (2 x 128 x D bf16).
+    static constexpr int kNSTkv = 3;
+    static constexpr int kDkvStage = 2 * kTile64;
+    static constexpr int kAux = 528;
+    static constexpr int kDkvSmem = 1024 + 2 * kTile128 + kNSTkv * kDkvStage + 2 * kTile128 + kNSTkv * kAux;
+    // dq: resident Q, dO (128 rows); kNSTq stages of K64, V64; staging for dQ (128 x D)
+    static constexpr int kNSTq = 4;
     static constexpr int kDqStage = 2 * kTile64;
-    static constexpr int kDqSmem = 1024 + 2 * kTile128 + kNST * kDqStage;
+    static constexpr int kDqSmem = 1024 + 2 * kTile128 + kNSTq * kDqStage + kTile128;
 };
 
 // Stage layout of the dK/dV kernel: Q rows [64][D] | dO rows [64][D] |
@@ -102,10 +105,11 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     s2_bwd_dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                       const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                      const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
                       const BwdParams p) {
     using C = BwdCfg<D>;
-    constexpr int NST = C::kNST;
-    constexpr int kMeta = 2 * C::kTile64 + 512;  // byte offset of a stage's meta
+    constexpr int NST = C::kNSTkv;
+    constexpr int kMeta = 512;  // byte offset of the meta in a stage's aux slot
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -114,7 +118,9 @@ __global__ void __launch_bounds__(384, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sK = smem_u32(smem), sV = sK + C::kTile128;
     const uint32_t sSt = sV + C::kTile128;
-    uint8_t* const gSt = smem + 2 * C::kTile128;  // generic pointer to stage 0
+    const uint32_t sOut = sSt + NST * C::kDkvStage;  // [wg: dV, dK][chunk][D/64][64 rows][128 B]
+    const uint32_t sAux = sOut + 2 * C::kTile128;
+    uint8_t* const gAux = smem + (sAux - sK);  // generic pointer to aux 0
     const BwdItem* items = static_cast<const BwdItem*>(p.items);
     const BwdEntry* ents = static_cast<const BwdEntry*>(p.entries);
 
@@ -157,12 +163,13 @@ __global__ void __launch_bounds__(384, 1)
                 const BwdItem it = items[i];
                 if (it_cnt > 0) mbar_wait(smem_u32(&bar_kve), (it_cnt - 1) & 1);
                 const int nc = it.c1 >= 0 ? 2 : 1;
-                mbar_expect_tx(smem_u32(&bar_kvf), 2 * nc * C::kSub * 8192);
+                const uint32_t kvbar = smem_u32(&bar_kvf);
+                mbar_expect_tx(kvbar, 2 * nc * C::kSub * 8192);
                 for (int h = 0; h < nc; ++h)
                     for (int s = 0; s < C::kSub; ++s) {
                         const int row = (h ? it.c1 : it.c0) * 64;
-                        tma_load_3d(sK + s * 16384 + h * 8192, &tmK, smem_u32(&bar_kvf), s * 64, row, it.kvbh);
-                        tma_load_3d(sV + s * 16384 + h * 8192, &tmV, smem_u32(&bar_kvf), s * 64, row, it.kvbh);
+                        tma_load_3d(sK + s * 16384 + h * 8192, &tmK, kvbar, s * 64, row, it.kvbh);
+                        tma_load_3d(sV + s * 16384 + h * 8192, &tmV, kvbar, s * 64, row, it.kvbh);
                     }
                 for (int j = 0; j < p.hpg; ++j) {
                     const int qbh = it.kvbh * p.hpg + j;
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(384, 1)
                             const uint32_t base = sSt + st * C::kDkvStage;
                             const uint32_t bar = smem_u32(&bar_sf[st]);
                             const int row0 = en.qtile * 128 + half * 64;
-                            *reinterpret_cast<uint4*>(gSt + st * C::kDkvStage + kMeta) =
+                            *reinterpret_cast<uint4*>(gAux + st * C::kAux + kMeta) =
                                 make_uint4(static_cast<uint32_t>(row0), m0, m1, static_cast<uint32_t>(qbh));
                             mbar_expect_tx(bar, 2 * C::kTile64 + 512);
                             for (int s = 0; s < C::kSub; ++s) {
@@ -185,8 +192,8 @@ __global__ void __launch_bounds__(384, 1)
                                 tma_load_3d(base + C::kTile64 + s * 8192, &tmdO, bar, s * 64, row0, qbh);
                             }
                             const size_t lo = static_cast<size_t>(qbh) * p.Npad + row0;
-                            bulk_load(base + 2 * C::kTile64, p.lse2 + lo, 256, bar);
-                            bulk_load(base + 2 * C::kTile64 + 256, p.delta + lo, 256, bar);
+                            bulk_load(sAux + st * C::kAux, p.lse2 + lo, 256, bar);
+                            bulk_load(sAux + st * C::kAux + 256, p.delta + lo, 256, bar);
                             ++st_it;
                         }
                     }
@@ -214,7 +221,11 @@ __global__ void __launch_bounds__(384, 1)
                     S2TRACE(3, n);
                     mbar_wait(smem_u32(&bar_p[b]), (n >> 1) & 1);
                     S2TRACE(4, n);
-                    if (first && it_cnt > 0) mbar_wait(smem_u32(&bar_ae), (it_cnt - 1) & 1);
+                    if (first && it_cnt > 0) {
+                        S2TRACE(11, it_cnt);
+                        mbar_wait(smem_u32(&bar_ae), (it_cnt - 1) & 1);
+                        S2TRACE(12, it_cnt);
+                    }
                     tc_fence_after();  // A operands (P^T, dS^T) were written to TMEM by tcgen05.st
                     const uint64_t dst = dStMN0 + static_cast<uint64_t>((st * C::kDkvStage) >> 4);
                     if (leader) {
@@ -299,10 +310,9 @@ __global__ void __launch_bounds__(384, 1)
                 // observe the stage barrier ourselves (already complete; the
                 // stage cannot be refilled before our P arrives).
                 mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
-                const uint32_t sbase = sSt + st * C::kDkvStage;
-                const uint4 meta = *reinterpret_cast<const uint4*>(gSt + st * C::kDkvStage + kMeta);
+                const uint4 meta = *reinterpret_cast<const uint4*>(gAux + st * C::kAux + kMeta);
                 const uint32_t m = key_ok ? (hk ? meta.z : meta.y) : 0u;
-                const uint32_t sl = sbase + 2 * C::kTile64 + wg * 128;
+                const uint32_t sl = sAux + st * C::kAux + wg * 128;
                 const bool on0 = (m >> (wg * 8 + cg)) & 1u;
                 const bool on1 = (m >> (wg * 8 + 4 + cg)) & 1u;
                 const int q0 = static_cast<int>(meta.x) + wg * 32;
@@ -351,29 +361,50 @@ __global__ void __launch_bounds__(384, 1)
                 if (tid == 128) S2TRACE(7, st_it);
             }
             // ---------------------------------------------------- epilogue
+            // TMEM -> registers (then the accumulators are released), bf16 into
+            // the swizzled staging tile, TMA stores (one 64 x 64 box per chunk
+            // and D/64 slice; rows past seq_len are clipped by the tensor map).
+            if (tid == 128) S2TRACE(8, it_cnt);
             mbar_wait(smem_u32(&bar_af), it_cnt & 1);
+            if (tid == 128) S2TRACE(9, it_cnt);
             tc_fence_after();
             const float mul = wg ? p.scale : 1.0f;  // wg0 -> dV, wg1 -> dK
-            __nv_bfloat16* dst = (wg ? p.g0 : p.g1) + (static_cast<size_t>(it.kvbh) * p.N + key_pos) * D;
+            uint32_t acc[D];
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                uint32_t u[32];
-                tmem_ld32(tmem + (wg ? 384 : 256) + c * 32 + lane_off, u);
-                tmem_ld_wait();
-                if (key_ok) {
-                    uint4 w[4];
-                    uint32_t* wp = reinterpret_cast<uint32_t*>(w);
-#pragma unroll
-                    for (int q = 0; q < 16; ++q)
-                        wp[q] = pack_bf16(__uint_as_float(u[2 * q]) * mul, __uint_as_float(u[2 * q + 1]) * mul);
-                    uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) d4[q] = w[q];
-                }
-            }
+            for (int c = 0; c < D / 32; ++c)
+                tmem_ld32(tmem + (wg ? 384 : 256) + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(acc + 32 * c));
+            tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(smem_u32(&bar_ae));
+            const bool wg_leader = (tid & 127) == 0;
+            if (wg_leader) bulk_wait_read0();  // previous item's stores have read the staging tile
+            named_bar_sync(1 + wg, 128);
+            const uint32_t so = sOut + wg * C::kTile128 + hk * (C::kSub * 8192) + (kr & 63) * 128;
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) {  // 16-byte chunk c of the row: D/64 slice c>>3
+                const uint32_t w0 = pack_bf16(__uint_as_float(acc[8 * c]) * mul, __uint_as_float(acc[8 * c + 1]) * mul);
+                const uint32_t w1 = pack_bf16(__uint_as_float(acc[8 * c + 2]) * mul, __uint_as_float(acc[8 * c + 3]) * mul);
+                const uint32_t w2 = pack_bf16(__uint_as_float(acc[8 * c + 4]) * mul, __uint_as_float(acc[8 * c + 5]) * mul);
+                const uint32_t w3 = pack_bf16(__uint_as_float(acc[8 * c + 6]) * mul, __uint_as_float(acc[8 * c + 7]) * mul);
+                sts_u4(so + (c >> 3) * 8192 + (((c & 7) ^ (kr & 7)) << 4), w0, w1, w2, w3);
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1 + wg, 128);
+            if (wg_leader) {
+                const CUtensorMap* tm = wg ? &tmdK : &tmdV;
+                for (int h = 0; h < 2; ++h) {
+                    const int ch = h ? it.c1 : it.c0;
+                    if (ch < 0) continue;
+#pragma unroll
+                    for (int sb = 0; sb < C::kSub; ++sb)
+                        tma_store_3d(tm, sOut + wg * C::kTile128 + h * (C::kSub * 8192) + sb * 8192, sb * 64,
+                                     ch * 64, it.kvbh);
+                }
+                bulk_commit();
+            }
+            if (tid == 128) S2TRACE(10, it_cnt);
         }
+        if ((tid & 127) == 0) bulk_wait0();  // staging tiles must outlive the stores
     }
     tc_fence_before();
     __syncthreads();
@@ -387,9 +418,10 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     s2_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                     const __grid_constant__ CUtensorMap tmdQ, const __grid_constant__ CUtensorMap /*unused*/,
                      const BwdParams p) {
     using C = BwdCfg<D>;
-    constexpr int NST = C::kNST;
+    constexpr int NST = C::kNSTq;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -398,6 +430,7 @@ __global__ void __launch_bounds__(384, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sQ = smem_u32(smem), sdO = sQ + C::kTile128;
     const uint32_t sSt = sdO + C::kTile128;
+    const uint32_t sOut = sSt + NST * C::kDqStage;  // dQ staging [D/64][128 rows][128 B]
     const FwdItem* items = static_cast<const FwdItem*>(p.items);
     const int2* chunks = static_cast<const int2*>(p.entries);
 
@@ -439,10 +472,11 @@ __global__ void __launch_bounds__(384, 1)
                 const FwdItem it = items[i];
                 const int kvbh = it.bh / p.hpg;
                 if (it_cnt > 0) mbar_wait(smem_u32(&bar_qe), (it_cnt - 1) & 1);
-                mbar_expect_tx(smem_u32(&bar_qf), 2 * C::kTile128);
+                const uint32_t qbar = smem_u32(&bar_qf);
+                mbar_expect_tx(qbar, 2 * C::kTile128);
                 for (int s = 0; s < C::kSub; ++s) {
-                    tma_load_3d(sQ + s * 16384, &tmQ, smem_u32(&bar_qf), s * 64, it.qtile * 128, it.bh);
-                    tma_load_3d(sdO + s * 16384, &tmdO, smem_u32(&bar_qf), s * 64, it.qtile * 128, it.bh);
+                    tma_load_3d(sQ + s * 16384, &tmQ, qbar, s * 64, it.qtile * 128, it.bh);
+                    tma_load_3d(sdO + s * 16384, &tmdO, qbar, s * 64, it.qtile * 128, it.bh);
                 }
                 for (int n = 0; n < it.chunk_cnt; ++n, ++st_it) {
                     const int st = st_it % NST;
@@ -473,7 +507,9 @@ __global__ void __launch_bounds__(384, 1)
                 bool first = true;
                 auto accumulate = [&](uint32_t n, int st) {
                     const int b = n & 1;
+                    S2TRACE(3, n);
                     mbar_wait(smem_u32(&bar_p[b]), (n >> 1) & 1);
+                    S2TRACE(4, n);
                     if (first && it_cnt > 0) mbar_wait(smem_u32(&bar_ae), (it_cnt - 1) & 1);
                     tc_fence_after();  // A operand (dS) was written to TMEM by tcgen05.st
                     const uint64_t dst = dStMN0 + static_cast<uint64_t>((st * C::kDqStage) >> 4);
@@ -491,7 +527,9 @@ __global__ void __launch_bounds__(384, 1)
                 uint32_t prev_n = 0;
                 for (int n = 0; n < chunk_cnt; ++n, ++st_it, ++n_glob) {
                     const int st = st_it % NST;
+                    S2TRACE(0, n_glob);
                     mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
+                    S2TRACE(1, n_glob);
                     const uint64_t dst = dSt0 + static_cast<uint64_t>((st * C::kDqStage) >> 4);
                     const int b = n_glob & 1;
                     if (leader) {
@@ -503,16 +541,19 @@ __global__ void __launch_bounds__(384, 1)
                             mma_ss(tmem + 128 + b * 64, ddO0 + ao, dst + ((C::kTile64 >> 4) + bo), idS, kk > 0);
                         }
                         mma_commit(smem_u32(&bar_s[b]));
+                        // Q / dO feed only S / dP: release them after the item's last ones
+                        if (n == chunk_cnt - 1) mma_commit(smem_u32(&bar_qe));
                     }
                     __syncwarp();
+                    S2TRACE(2, n_glob);
                     if (prev_st >= 0) accumulate(prev_n, prev_st);
                     prev_st = st;
                     prev_n = n_glob;
                 }
                 if (prev_st >= 0) accumulate(prev_n, prev_st);
                 if (leader) {
+                    if (chunk_cnt == 0) mma_commit(smem_u32(&bar_qe));  // (user CSR with empty rows)
                     mma_commit(smem_u32(&bar_af));
-                    mma_commit(smem_u32(&bar_qe));
                 }
                 __syncwarp();
             }
@@ -534,7 +575,9 @@ __global__ void __launch_bounds__(384, 1)
             for (int n = 0; n < it.chunk_cnt; ++n, ++n_glob) {
                 const int2 ch = chunks[it.chunk_off + n];
                 const int b = n_glob & 1;
+                if (tid == 128) S2TRACE(5, n_glob);
                 mbar_wait(smem_u32(&bar_s[b]), (n_glob >> 1) & 1);
+                if (tid == 128) S2TRACE(6, n_glob);
                 tc_fence_after();
                 uint32_t su[32], du[32];
                 tmem_ld32(tmem + b * 64 + wg * 32 + lane_off, su);
@@ -570,31 +613,42 @@ __global__ void __launch_bounds__(384, 1)
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(smem_u32(&bar_p[b]));
+                if (tid == 128) S2TRACE(7, n_glob);
             }
             mbar_wait(smem_u32(&bar_af), it_cnt & 1);
             tc_fence_after();
-            const bool valid = q_pos < p.N;
-            __nv_bfloat16* dst = p.g0 + (static_cast<size_t>(it.bh) * p.N + q_pos) * D + wg * (D / 2);
+            // TMEM -> registers (accumulator released), bf16 into the swizzled
+            // staging tile, TMA store of the 128 x D tile (rows past seq_len clipped)
+            uint32_t acc[D / 2];
 #pragma unroll
-            for (int c = 0; c < D / 64; ++c) {
-                uint32_t u[32];
-                tmem_ld32(tmem + 256 + wg * (D / 2) + c * 32 + lane_off, u);
-                tmem_ld_wait();
-                if (valid) {
-                    uint4 w[4];
-                    uint32_t* wp = reinterpret_cast<uint32_t*>(w);
-#pragma unroll
-                    for (int q = 0; q < 16; ++q)
-                        wp[q] = pack_bf16(__uint_as_float(u[2 * q]) * p.scale,
-                                          __uint_as_float(u[2 * q + 1]) * p.scale);
-                    uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) d4[q] = w[q];
-                }
-            }
+            for (int c = 0; c < D / 64; ++c)
+                tmem_ld32(tmem + 256 + wg * (D / 2) + c * 32 + lane_off,
+                          *reinterpret_cast<uint32_t(*)[32]>(acc + 32 * c));
+            tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(smem_u32(&bar_ae));
+            if (tid == 128) bulk_wait_read0();  // previous item's store has read the staging tile
+            named_bar_sync(1, 256);
+            const float sc = it.chunk_cnt > 0 ? p.scale : 0.f;  // no chunks: dQ = 0
+#pragma unroll
+            for (int c = 0; c < D / 16; ++c) {  // my 16-byte chunks: global chunk index g
+                const int g = wg * (D / 16) + c;
+                const uint32_t w0 = pack_bf16(__uint_as_float(acc[8 * c]) * sc, __uint_as_float(acc[8 * c + 1]) * sc);
+                const uint32_t w1 = pack_bf16(__uint_as_float(acc[8 * c + 2]) * sc, __uint_as_float(acc[8 * c + 3]) * sc);
+                const uint32_t w2 = pack_bf16(__uint_as_float(acc[8 * c + 4]) * sc, __uint_as_float(acc[8 * c + 5]) * sc);
+                const uint32_t w3 = pack_bf16(__uint_as_float(acc[8 * c + 6]) * sc, __uint_as_float(acc[8 * c + 7]) * sc);
+                sts_u4(sOut + (g >> 3) * 16384 + r * 128 + (((g & 7) ^ (r & 7)) << 4), w0, w1, w2, w3);
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1, 256);
+            if (tid == 128) {
+#pragma unroll
+                for (int sb = 0; sb < C::kSub; ++sb)
+                    tma_store_3d(&tmdQ, sOut + sb * 16384, sb * 64, it.qtile * 128, it.bh);
+                bulk_commit();
+            }
         }
+        if (tid == 128) bulk_wait0();  // the staging tile must outlive the store
     }
     tc_fence_before();
     __syncthreads();
@@ -627,30 +681,33 @@ cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* do
 template <class K>
 static cudaError_t launch_bwd(K kern, int smem, int grid, const CUtensorMap& q,
                               const CUtensorMap& dout, const CUtensorMap& k, const CUtensorMap& v,
-                              const BwdParams& p, cudaStream_t stream) {
+                              const CUtensorMap& o0, const CUtensorMap& o1, const BwdParams& p,
+                              cudaStream_t stream) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 384, smem, stream>>>(q, dout, k, v, p);
+    kern<<<grid, 384, smem, stream>>>(q, dout, k, v, o0, o1, p);
     return cudaGetLastError();
 }
 
-// which = 0: dK/dV kernel (q/do: 64-row boxes); which = 1: dQ kernel (q/do:
-// 128-row boxes).  k/v: 64-row boxes.
+// which = 0: dK/dV kernel (q/do: 64-row boxes; o0 = dK, o1 = dV maps with 64-row
+// boxes); which = 1: dQ kernel (q/do: 128-row boxes; o0 = dQ map, 128-row boxes).
+// k/v: 64-row boxes.
 cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CUtensorMap& dout,
-                                const CUtensorMap& k, const CUtensorMap& v, const void* items,
-                                const int* sched, int grid, const void* entries,
-                                const float* lse2, const float* delta, __nv_bfloat16* g0,
-                                __nv_bfloat16* g1, int N, int Npad, int hpg, float scale,
-                                cudaStream_t stream) {
+                                const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o0,
+                                const CUtensorMap& o1, const void* items, const int* sched, int grid,
+                                const void* entries, const float* lse2, const float* delta,
+                                int N, int Npad, int hpg, float scale, cudaStream_t stream) {
     if (grid == 0) return cudaSuccess;
     const float sl2 = scale * 1.4426950408889634f;
-    BwdParams pp{items, sched, entries, lse2, delta, g0, g1, N, Npad, hpg, sl2, scale, g_trace, g_debug};
+    // debug bit 8 selects which kernel records the trace (0: dK/dV, 8: dQ)
+    long long* tr = ((g_debug & 8) != 0) == (which == 1) ? g_trace : nullptr;
+    BwdParams pp{items, sched, entries, lse2, delta, nullptr, nullptr, N, Npad, hpg, sl2, scale, tr, g_debug & 7};
     if (g_debug & 4) grid = 1;  // debug: isolate one CTA from memory-system contention
     if (D == 128)
-        return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<128>, BwdCfg<128>::kDkvSmem, grid, q, dout, k, v, pp, stream)
-                          : launch_bwd(s2_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmem, grid, q, dout, k, v, pp, stream);
+        return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<128>, BwdCfg<128>::kDkvSmem, grid, q, dout, k, v, o0, o1, pp, stream)
+                          : launch_bwd(s2_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmem, grid, q, dout, k, v, o0, o1, pp, stream);
     if (D == 64)
-        return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<64>, BwdCfg<64>::kDkvSmem, grid, q, dout, k, v, pp, stream)
-                          : launch_bwd(s2_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmem, grid, q, dout, k, v, pp, stream);
+        return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<64>, BwdCfg<64>::kDkvSmem, grid, q, dout, k, v, o0, o1, pp, stream)
+                          : launch_bwd(s2_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmem, grid, q, dout, k, v, o0, o1, pp, stream);
     return cudaErrorInvalidValue;
 }

@@ -29,6 +29,8 @@ for _ in range(3):
 torch.cuda.synchronize()
 import ctypes
 L = s2.lib()
+L.s2_debug_set_mode.argtypes = [ctypes.c_int]
+L.s2_debug_set_mode(int(os.environ.get("S2_DEBUG", "0")))  # kernel ablations (results invalid when != 0)
 L.s2_profile_enable(1)
 tf = tb = 0.0
 for _ in range(a.iters):

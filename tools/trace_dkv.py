@@ -1,4 +1,5 @@
-"""Debug: CTA-0 per-step timeline of the dK/dV kernel (s2_debug_set_trace)."""
+"""Debug: CTA-0 per-step timeline of the dK/dV kernel, or of the dQ kernel with
+`dq` as the second argument (s2_debug_set_trace; the other kernel runs untraced)."""
 import ctypes
 import os
 import sys
@@ -18,12 +19,12 @@ out, lse = s2.s2_attn_fwd(plan, q, k, v)
 s2.s2_attn_bwd(plan, q, k, v, out, lse, do)
 L.s2_debug_set_mode.argtypes = [ctypes.c_int]
 L.s2_debug_set_mode(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
-tr = torch.zeros(8 * 2048, dtype=torch.int64, device="cuda")
+tr = torch.zeros(16 * 2048, dtype=torch.int64, device="cuda")
 L.s2_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
 s2.s2_attn_bwd(plan, q, k, v, out, lse, do)
 torch.cuda.synchronize()
 L.s2_debug_set_trace(None)
-t = tr.cpu().numpy().reshape(8, 2048)
+t = tr.cpu().numpy().reshape(16, 2048)
 n = int((t[2] > 0).sum())
 t0 = t[0, 0]
 t = t - t0
@@ -41,3 +42,17 @@ print("median MMA wait p:", np.median(t[4, 10:n - 1] - t[3, 10:n - 1]))
 print("median MMA wait stage:", np.median(t[1, 10:n] - t[0, 10:n]))
 print("median S issue->EW sees S:", np.median(t[6, 10:n] - t[2, 10:n]))
 print("median EW arrive->MMA sees P:", np.median(t[4, 10:n - 1] - t[7, 10:n - 1]))
+dd = np.diff(t[2, 1:n]).astype(np.float64)
+print(f"mean cycles/step {dd.mean():.0f}  (median {np.median(dd):.0f}); steps > 2x median: {(dd > 2 * np.median(dd)).sum()} "
+      f"carrying {dd[dd > 2 * np.median(dd)].sum() / dd.sum():.1%} of the time")
+long = np.where(dd > 2 * np.median(dd))[0] + 1  # index of the step whose S commit came late
+ws = (t[1] - t[0]).astype(np.float64)
+wp = (t[4] - t[3]).astype(np.float64)
+iss = (t[2] - t[1]).astype(np.float64)
+print("long steps: median wait_sf", np.median(ws[long]), " issue S", np.median(iss[long]),
+      " wait_p(prev)", np.median(wp[long - 1]), " gap", np.median(dd[long - 1]))
+ni = int((t[10] != -t0).sum())
+if ni > 2:
+    e = t[:, 1:ni - 1].astype(np.float64)
+    print(f"items traced {ni}: EW wait af {np.median(e[9] - e[8]):.0f}, epilogue {np.median(e[10] - e[9]):.0f}; "
+          f"MMA wait ae {np.median(e[12] - e[11]):.0f}")
