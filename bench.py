@@ -41,6 +41,19 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture (tools/ncu_summary.py traffic), or None."""
+    try:
+        with open(TRAFFIC_PATH) as f:
+            return json.load(f)[kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -296,7 +309,8 @@ def run_s2(args):
     if dom:
         ach = alg.get(dom, 0.0) / (kernels[dom]["avg_ms"] * 1e-3) / 1e12
         roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"],
-                "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops"], "traffic": None,
+                "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops"], "traffic": ncu_traffic(dom),
+                "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read+write per launch, ncu --set full)",
                 "peak_source": f"{pk_kind} bf16_tflops (burst)",
                 "frac_of_sustained": ach / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
                 "alg_flops_per_launch": alg.get(dom, 0.0)}
@@ -438,7 +452,7 @@ def bench_decode(args, dev, world):
             "kernels": kern, "bytes_per_step": by, "pool_bytes": pool, "dense_cache_bytes": dense,
             "roofline": {"kernel": "decode_split", "bound": "hbm", "achieved": ach,
                          "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
-                         "frac_of_8TBps": ach / 8000.0, "traffic": None,
+                         "frac_of_8TBps": ach / 8000.0, "traffic": ncu_traffic("decode_split"),
                          "peak_source": f"{pk_kind} hbm_gbs"},
             "e2e": {"value": world * Bd / (ems * 1e-3), "unit": "tok/s", "ms_per_step": ems,
                     "h2d_bytes_per_step": q.numel() * 2, "d2h_bytes_per_step": out.numel() * 2}}

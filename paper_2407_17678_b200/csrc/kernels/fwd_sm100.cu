@@ -376,8 +376,8 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 m_run = m_use;
                 const float base = (m_use == -INFINITY) ? 0.f : m_use;
-                // P = 2^(S*scale*log2e - m): packed FFMA2, 3/4 of the pairs on MUFU.EX2 and
-                // 1/4 on the FMA pipe (exp2_poly2) so the XU pipe stops pacing the tile
+                // P = 2^(S*scale*log2e - m): packed FFMA2, half of the pairs on MUFU.EX2 and
+                // half on the FMA pipe (exp2_poly2) so the XU pipe stops pacing the tile
                 const uint64_t sl2v = f2_pack(sl2, sl2), nbase = f2_pack(-base, -base);
                 uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};  // +0.0f pairs; 4 independent chains
 #pragma unroll
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(384, 1)
                         for (int j = 0; j < 16; ++j) {
                             const uint64_t x = ffma2(f2_pack(sv[c * 32 + 2 * j], sv[c * 32 + 2 * j + 1]), sl2v, nbase);
                             uint64_t pr;
-                            if ((j & 3) == 3) {
+                            if ((j & 1) == 1) {
                                 pr = exp2_poly2(x);
                             } else {
                                 float x0, x1;

@@ -2,7 +2,12 @@
 
     python tools/ncu_summary.py launches gpurun_out/launches.csv
     python tools/ncu_summary.py report gpurun_out/prof.ncu-rep [alg_flops_per_launch]
+    python tools/ncu_summary.py traffic out.json rep1.ncu-rep [rep2.ncu-rep ...]
+        per-kernel DRAM bytes (read + write) per launch from --set full captures,
+        keyed by the names bench.py profiles under (read by bench.py for
+        roofline.traffic)
 """
+import json
 import collections
 import csv
 import io
@@ -80,8 +85,40 @@ def report(path, alg=None):
         print()
 
 
+BENCH_NAMES = {"s2_fwd_sm100_kernel": "fwd_sm100", "s2_bwd_dkv_kernel": "bwd_dkv_sm100",
+               "s2_bwd_dq_kernel": "bwd_dq_sm100", "s2_bwd_prep_kernel": "bwd_prep",
+               "s2_decode_split_kernel": "decode_split", "s2_decode_combine_kernel": "decode_combine"}
+
+
+def traffic(out_path, reps):
+    res = {}
+    for path in reps:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        hdr, units = rows[0], rows[1]
+        for vals in rows[2:]:
+            full = vals[hdr.index("Kernel Name")]
+            key = next((v for k, v in BENCH_NAMES.items() if k in full), None)
+            if key is None:
+                continue
+
+            def val(m):
+                i = hdr.index(m)
+                f = float(vals[i].replace(",", ""))
+                return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                            "ms": 1e-3, "msecond": 1e-3, "us": 1e-6, "usecond": 1e-6,
+                            "ns": 1e-9, "nsecond": 1e-9}.get(units[i], 1)
+            res[key] = {"dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
+                        "duration_s_under_ncu": val("gpu__time_duration.sum"), "source": path.split("/")[-1]}
+    json.dump(res, open(out_path, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3:])
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2])
     else:
         report(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
