@@ -42,7 +42,14 @@ enum {
     S2_ERR_CUDA = 2,
     S2_ERR_UNSUPPORTED = 3,
     S2_ERR_NO_DEVICE = 4,
-    S2_ERR_OUT_OF_MEMORY = 5
+    S2_ERR_OUT_OF_MEMORY = 5,
+    /* load_config_file's std::runtime_error (serialize.cpp:123-146): the file
+     * cannot be opened / parsed, or a field is missing or invalid; the
+     * message names the file and the offending field. */
+    S2_ERR_CONFIG = 6,
+    /* a caller-provided output buffer is too small; the *len / count outputs
+     * carry the size needed */
+    S2_ERR_BUFFER_TOO_SMALL = 7
 };
 
 /* Message for the last non-zero status returned on this thread. */
@@ -247,6 +254,84 @@ int s2_stream_synchronize(s2_stream_t stream);
 int s2_profile_enable(int enable);
 int s2_profile_collect(int max_kernels, char* names, double* total_ms, int* launches,
                        int* num_kernels);
+
+/* ---- serialization (reference serialize.hpp / serialize.cpp) -----------
+ * JSON documents are UTF-8 text.  to_json outputs are the reference's
+ * canonical encoding (object keys sorted, compact separators), so
+ * s2_pattern_hash equals shardattn::config_hash for the same config. */
+
+/* to_json(PatternConfig) (serialize.cpp:30-47).  buf may be NULL (size
+ * query); *len = bytes excluding the terminating NUL. */
+int s2_pattern_to_json(const s2_pattern_config* cfg, char* buf, size_t cap, size_t* len);
+/* pattern_config_from_json (serialize.cpp:75-95): defaults num_kv_heads =
+ * num_heads, local_blocks = 1, local_stride = 1, offset_scheme
+ * "head_mod_stride"; validates (pattern.cpp:36-79).  Segment offsets are
+ * written to offsets_buf (offsets_cap ints) and cfg's offset pointers point
+ * into it. */
+int s2_pattern_from_json(const char* text, s2_pattern_config* cfg, int* offsets_buf,
+                         int offsets_cap);
+/* config_hash (serialize.cpp:148-156): FNV-1a 64 over the canonical document. */
+int s2_pattern_hash(const s2_pattern_config* cfg, uint64_t* hash);
+
+/* to_json(CsrMask) / csr_from_json (serialize.cpp:68-73,108-116); from_json
+ * validates (csr.cpp:11-33).  Pass NULL arrays to query num_blocks / nnz. */
+int s2_csr_to_json(int head_index, int num_blocks, const int* row_ptr, const int* col_idx,
+                   char* buf, size_t cap, size_t* len);
+int s2_csr_from_json(const char* text, int* head_index, int* num_blocks, int* row_ptr,
+                     int row_cap, int* col_idx, int64_t col_cap, int64_t* nnz);
+
+/* POD mirror of shardattn::LayerSchedule (pattern.hpp:98-104). */
+typedef struct s2_layer_schedule {
+    int num_layers;
+    int num_dense;
+    const int* dense_layer_ids; /* host pointer, ascending */
+    s2_pattern_config sparse_pattern;
+} s2_layer_schedule;
+/* LayerSchedule::validate (pattern.cpp:118-125). */
+int s2_schedule_validate(const s2_layer_schedule* schedule);
+/* to_json(LayerSchedule) / layer_schedule_from_json (serialize.cpp:49-53,97-106);
+ * from_json inherits default_pattern when "sparse_pattern" is absent. */
+int s2_schedule_to_json(const s2_layer_schedule* schedule, char* buf, size_t cap, size_t* len);
+int s2_schedule_from_json(const char* text, const s2_pattern_config* default_pattern,
+                          s2_layer_schedule* schedule, int* dense_buf, int dense_cap,
+                          int* offsets_buf, int offsets_cap);
+
+/* CliConfigFile / load_config_file (serialize.hpp:31-41, serialize.cpp:123-146):
+ * a pattern (top level or under "pattern"), an optional "schedule" and
+ * optional "report" {out, format}.  Failures -> S2_ERR_CONFIG with
+ * "config '<path>': <reason>" (file missing: "cannot open config file"). */
+typedef struct s2_config_file {
+    s2_pattern_config pattern;
+    int has_schedule;
+    s2_layer_schedule schedule; /* sparse_pattern == pattern unless given */
+    char out[512];
+    char format[64];
+} s2_config_file;
+int s2_config_file_load(const char* path, s2_config_file* file, int* dense_buf, int dense_cap,
+                        int* offsets_buf, int offsets_cap);
+
+/* ---- analysis (reference analysis.hpp / analysis.cpp) ------------------ */
+/* equivalent_context_length, analytic_flops_reduction, speedup_upper_bound
+ * (analysis.cpp:13-27); same argument checks. */
+int s2_equivalent_context_length(double seq_len, double local_window, double stride, double* out);
+int s2_analytic_flops_reduction(double seq_len, double local_window, double stride, double* out);
+int s2_speedup_upper_bound(int num_heads, double seq_len, double local_window, double* out);
+/* exact_flops (analysis.cpp:33-55): nnz_per_head may be NULL. */
+typedef struct s2_flops_report {
+    double dense_flops, sparse_flops, reduction_factor, equivalent_context;
+} s2_flops_report;
+int s2_exact_flops(const s2_pattern_config* cfg, int head_dim, s2_flops_report* report,
+                   int64_t* nnz_per_head);
+/* simulate_decode_cache for one head (analysis.cpp:57-104), computed from
+ * the CSC in O(B + total_tokens): evict_after[B], occupancy[total_tokens]
+ * (retained tokens per decode step), dead_blocks[total_tokens]; any output
+ * array may be NULL. */
+int s2_simulate_decode_cache(const s2_pattern_config* cfg, int total_tokens, int head,
+                             int* evict_after, int64_t* occupancy, int* dead_blocks,
+                             int64_t* peak_tokens, double* mean_tokens);
+/* kv_reduction (analysis.cpp:106-121): percent of KV cache saved vs dense,
+ * averaged over heads and layers (dense layers keep everything). */
+int s2_kv_reduction(const s2_layer_schedule* schedule, double* percent);
 
 #ifdef __cplusplus
 }

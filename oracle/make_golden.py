@@ -250,5 +250,108 @@ def main():
         json.dump({"rng": rng_fix, "cases": fwd}, f, indent=1)
 
 
+BAD_CONFIGS = {
+    # test_serialize.cpp:113-133 cases (the reference's message must name the field)
+    "missing_seq_len": '{"pattern": {"block_size": 64, "num_heads": 4}}',
+    "stride_zero": '{"seq_len": 64, "block_size": 8, "num_heads": 4, "stride_segments": '
+                   '[{"start_block_distance": 1, "end_block_distance": 8, "stride": 0}]}',
+    "unknown_scheme": '{"seq_len": 64, "block_size": 8, "num_heads": 4, "offset_scheme": "mystery"}',
+    "bad_dense_id": '{"seq_len": 512, "block_size": 64, "num_heads": 4, '
+                    '"schedule": {"num_layers": 4, "dense_layer_ids": [7]}}',
+    "not_json": '{"seq_len": 512, ',
+}
+GOOD_CONFIGS = {
+    # test_serialize.cpp:96-111
+    "with_schedule": '{"pattern": {"seq_len": 512, "block_size": 64, "num_heads": 4, "local_blocks": 1, '
+                     '"stride_segments": [{"start_block_distance": 1, "end_block_distance": 8, '
+                     '"stride": 2}]}, "schedule": {"num_layers": 12, "dense_layer_ids": [0]}, '
+                     '"report": {"out": "r.csv", "format": "csv"}}',
+    "bare": '{"seq_len": 64, "block_size": 8, "num_heads": 2}',
+    "schedule_own_pattern": '{"seq_len": 512, "block_size": 64, "num_heads": 4, "schedule": '
+                            '{"num_layers": 6, "dense_layer_ids": [5, 0], "sparse_pattern": '
+                            '{"seq_len": 512, "block_size": 64, "num_heads": 4, "local_blocks": 2, '
+                            '"stride_segments": [{"start_block_distance": 2, "end_block_distance": 8, '
+                            '"stride": 3, "offsets": [0, 1, 2, 0]}]}}}',
+}
+
+
+def serialize_fixtures(R):
+    """tests/golden/serialize.json: canonical documents, config hashes, config
+    files, kv_reduction, decode-cache schedules and analytic closed forms,
+    all produced by the reference library."""
+    import tempfile
+
+    out = {"patterns": {}, "config_files": {}, "kv_reduction": [], "decode_cache": {},
+           "analytic": []}
+    buf = ctypes.create_string_buffer(1 << 20)
+    for name, cfg in layout_configs().items():
+        c, keep = cfg.to_c()
+        if R.ref_validate(ctypes.byref(c)) != 0:
+            continue
+        assert R.ref_config_json(ctypes.byref(c), buf, len(buf)) == 0
+        h = ctypes.c_uint64()
+        assert R.ref_config_hash(ctypes.byref(c), ctypes.byref(h)) == 0
+        out["patterns"][name] = {"config": cfg_to_dict(cfg), "json": buf.value.decode(),
+                                 "hash": f"{h.value:016x}"}
+    texts = dict(GOOD_CONFIGS)
+    texts.update(BAD_CONFIGS)
+    for fn in sorted(os.listdir(REF_CONFIGS)) if os.path.isdir(REF_CONFIGS) else []:
+        with open(os.path.join(REF_CONFIGS, fn)) as f:
+            texts["refcfg_" + fn[:-5]] = f.read()
+    bufs = [ctypes.create_string_buffer(1 << 16) for _ in range(4)]
+    with tempfile.TemporaryDirectory() as d:
+        for name, text in texts.items():
+            path = os.path.join(d, name + ".json")
+            with open(path, "w") as f:
+                f.write(text)
+            rc = R.ref_load_config(path.encode(), *bufs, 1 << 16)
+            rec = {"text": text}
+            if rc == 0:
+                rec.update(pattern=bufs[0].value.decode(), schedule=bufs[1].value.decode(),
+                           out=bufs[2].value.decode(), format=bufs[3].value.decode())
+            else:
+                rec["error"] = R.ref_last_error().decode().replace(path, "<path>")
+            out["config_files"][name] = rec
+    sched = [("cfg3_32k", 24, [0, 1]), ("cfg2_llama7b_8k", 32, []), ("cfg4_decode_128k_gqa", 32, [0, 31]),
+             ("figure_left", 4, [1]), ("multi_stride", 12, [0, 5, 11]), ("refcfg_l1v15_dense01", 24, [0, 1]),
+             ("refcfg_swa576_dense01", 24, [0, 1]), ("block32_ragged", 3, [])]
+    cfgs = layout_configs()
+    for name, L, dense in sched:
+        c, keep = cfgs[name].to_c()
+        ids = np.array(dense or [0], np.int32)
+        pct = ctypes.c_double()
+        assert R.ref_kv_reduction(ctypes.byref(c), L, oracle.ip(ids), len(dense), ctypes.byref(pct)) == 0
+        out["kv_reduction"].append({"pattern": name, "num_layers": L, "dense": dense, "percent": pct.value})
+    for name in ("figure_left", "figure_right", "cfg1_fp32_2k", "gqa_explicit_offsets", "block32_ragged",
+                 "fuzz_03", "fuzz_11"):
+        cfg = cfgs[name]
+        c, keep = cfg.to_c()
+        T = min(cfg.seq_len, 2048)
+        heads = []
+        for h in range(min(cfg.num_heads, 3)):
+            ev = np.zeros(cfg.num_blocks(), np.int32)
+            occ = np.zeros(T, np.int64)
+            dead = np.zeros(T, np.int32)
+            pk, mean = ctypes.c_int64(), ctypes.c_double()
+            assert R.ref_decode_cache_full(ctypes.byref(c), T, h, oracle.ip(ev),
+                                           occ.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                           oracle.ip(dead), ctypes.byref(pk), ctypes.byref(mean)) == 0
+            heads.append({"evict_after": ev.tolist(), "occupancy": occ.tolist(), "dead": dead.tolist(),
+                          "peak": int(pk.value), "mean": mean.value})
+        out["decode_cache"][name] = {"config": cfg_to_dict(cfg), "total_tokens": T, "heads": heads}
+    for seq, lw, st, hh in ((32768, 256, 16, 32), (131072, 256, 16, 32), (8192, 64, 15, 16), (4096, 4096, 1, 1)):
+        eq, red, up = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        assert R.ref_analytic(seq, lw, st, hh, ctypes.byref(eq), ctypes.byref(red), ctypes.byref(up)) == 0
+        out["analytic"].append({"seq_len": seq, "local_window": lw, "stride": st, "num_heads": hh,
+                                "equivalent_context": eq.value, "reduction": red.value, "upper": up.value})
+    with open(os.path.join(GOLDEN, "serialize.json"), "w") as f:
+        json.dump(out, f, indent=0)
+    print(f"serialize fixtures: {len(out['patterns'])} patterns, {len(out['config_files'])} files")
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "serialize":
+        serialize_fixtures(oracle.ref())
+    else:
+        main()
+        serialize_fixtures(oracle.ref())

@@ -112,6 +112,13 @@ def ref():
             "ref_decode_cache": (ctypes.c_int, [C, ctypes.c_int, ctypes.c_int, _IP, _I64P, _IP]),
             "ref_kv_efficient": (ctypes.c_int, [C, ctypes.c_int, _IP]),
             "ref_exact_flops": (ctypes.c_int, [C, ctypes.c_int, _D, _D, _I64P]),
+            "ref_config_json": (ctypes.c_int, [C, ctypes.c_char_p, ctypes.c_int]),
+            "ref_config_hash": (ctypes.c_int, [C, ctypes.POINTER(ctypes.c_uint64)]),
+            "ref_load_config": (ctypes.c_int, [ctypes.c_char_p] * 5 + [ctypes.c_int]),
+            "ref_kv_reduction": (ctypes.c_int, [C, ctypes.c_int, _IP, ctypes.c_int, _D]),
+            "ref_decode_cache_full": (ctypes.c_int, [C, ctypes.c_int, ctypes.c_int, _IP, _I64P, _IP,
+                                                     _I64P, _D]),
+            "ref_analytic": (ctypes.c_int, [ctypes.c_double] * 3 + [ctypes.c_int, _D, _D, _D]),
             "ref_max_relative_error_f": (ctypes.c_double, [_F, _F, ctypes.c_int64]),
             "ref_max_relative_error_d": (ctypes.c_double, [_D, _D, ctypes.c_int64]),
         }

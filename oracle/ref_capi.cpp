@@ -21,6 +21,7 @@
 #include "shardattn/csr.hpp"
 #include "shardattn/pattern.hpp"
 #include "shardattn/selftest.hpp"
+#include "shardattn/serialize.hpp"
 #include "shardattn/verify.hpp"
 
 using namespace shardattn;
@@ -227,4 +228,63 @@ double ref_max_relative_error_d(const double* a, const double* b, int64_t n) {
     return max_relative_error(std::vector<double>(a, a + n), std::vector<double>(b, b + n));
 }
 
+
+// ---- serialize.cpp / analysis.cpp (fixtures for tests/test_serialize.py) ----
+static int put_str(const std::string& s, char* buf, int cap) {
+    if (!buf || cap < static_cast<int>(s.size()) + 1) throw std::length_error("buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+int ref_config_json(const s2_pattern_config* c, char* buf, int cap) {
+    return guarded([&] { put_str(to_json(to_cfg(c)).dump(), buf, cap); });
+}
+
+int ref_config_hash(const s2_pattern_config* c, uint64_t* h) {
+    return guarded([&] { *h = config_hash(to_cfg(c)); });
+}
+
+// load_config_file: canonical pattern / schedule documents, report fields.
+int ref_load_config(const char* path, char* pattern, char* schedule, char* out, char* format, int cap) {
+    return guarded([&] {
+        const CliConfigFile f = load_config_file(path);
+        put_str(to_json(f.pattern).dump(), pattern, cap);
+        put_str(f.schedule ? to_json(*f.schedule).dump() : std::string(), schedule, cap);
+        put_str(f.out, out, cap);
+        put_str(f.format, format, cap);
+    });
+}
+
+int ref_kv_reduction(const s2_pattern_config* c, int num_layers, const int* dense, int ndense,
+                     double* pct) {
+    return guarded([&] {
+        LayerSchedule s;
+        s.num_layers = num_layers;
+        for (int i = 0; i < ndense; ++i) s.dense_layer_ids.insert(dense[i]);
+        s.sparse_pattern = to_cfg(c);
+        *pct = kv_reduction(s);
+    });
+}
+
+int ref_decode_cache_full(const s2_pattern_config* c, int total_tokens, int head, int* evict_after,
+                          int64_t* occupancy, int* dead, int64_t* peak, double* mean) {
+    return guarded([&] {
+        const CacheSchedule cs = simulate_decode_cache(to_cfg(c), total_tokens);
+        const HeadCacheSchedule& h = cs.heads.at(head);
+        std::copy(h.evict_after.begin(), h.evict_after.end(), evict_after);
+        std::copy(h.occupancy.begin(), h.occupancy.end(), occupancy);
+        std::copy(h.dead_blocks.begin(), h.dead_blocks.end(), dead);
+        *peak = h.peak_tokens;
+        *mean = h.mean_tokens;
+    });
+}
+
+int ref_analytic(double seq_len, double local_window, double stride, int heads, double* eq,
+                 double* red, double* upper) {
+    return guarded([&] {
+        *eq = equivalent_context_length(seq_len, local_window, stride);
+        *red = analytic_flops_reduction(seq_len, local_window, stride);
+        *upper = speedup_upper_bound(heads, seq_len, local_window);
+    });
+}
 }  // extern "C"

@@ -15,6 +15,8 @@ S2_ERR_CUDA = 2
 S2_ERR_UNSUPPORTED = 3
 S2_ERR_NO_DEVICE = 4
 S2_ERR_OUT_OF_MEMORY = 5
+S2_ERR_CONFIG = 6
+S2_ERR_BUFFER_TOO_SMALL = 7
 S2_MAX_SEGMENTS = 8
 
 S2_DTYPE_BF16 = 0
@@ -33,6 +35,23 @@ class s2_pattern_config(ctypes.Structure):
                 ("local_blocks", ctypes.c_int), ("local_stride", ctypes.c_int),
                 ("num_segments", ctypes.c_int),
                 ("segments", s2_stride_segment * S2_MAX_SEGMENTS)]
+
+
+class s2_layer_schedule(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_int), ("num_dense", ctypes.c_int),
+                ("dense_layer_ids", ctypes.POINTER(ctypes.c_int)),
+                ("sparse_pattern", s2_pattern_config)]
+
+
+class s2_config_file(ctypes.Structure):
+    _fields_ = [("pattern", s2_pattern_config), ("has_schedule", ctypes.c_int),
+                ("schedule", s2_layer_schedule), ("out", ctypes.c_char * 512),
+                ("format", ctypes.c_char * 64)]
+
+
+class s2_flops_report(ctypes.Structure):
+    _fields_ = [("dense_flops", ctypes.c_double), ("sparse_flops", ctypes.c_double),
+                ("reduction_factor", ctypes.c_double), ("equivalent_context", ctypes.c_double)]
 
 
 class s2_plan_stats(ctypes.Structure):
@@ -66,6 +85,9 @@ _I = ctypes.c_int
 _I64P = ctypes.POINTER(ctypes.c_int64)
 _IP = ctypes.POINTER(ctypes.c_int)
 _CFG = ctypes.POINTER(s2_pattern_config)
+_SCH = ctypes.POINTER(s2_layer_schedule)
+_SZP = ctypes.POINTER(ctypes.c_size_t)
+_DP = ctypes.POINTER(ctypes.c_double)
 SIGNATURES = {
     "s2_last_error": (ctypes.c_char_p, []),
     "s2_abi_version": (_I, []),
@@ -112,6 +134,21 @@ SIGNATURES = {
     "s2_memcpy_h2d": (_I, [_P, _P, ctypes.c_size_t, _P]),
     "s2_memcpy_d2h": (_I, [_P, _P, ctypes.c_size_t, _P]),
     "s2_stream_synchronize": (_I, [_P]),
+    "s2_pattern_to_json": (_I, [_CFG, ctypes.c_char_p, ctypes.c_size_t, _SZP]),
+    "s2_pattern_from_json": (_I, [ctypes.c_char_p, _CFG, _IP, _I]),
+    "s2_pattern_hash": (_I, [_CFG, ctypes.POINTER(ctypes.c_uint64)]),
+    "s2_csr_to_json": (_I, [_I, _I, _IP, _IP, ctypes.c_char_p, ctypes.c_size_t, _SZP]),
+    "s2_csr_from_json": (_I, [ctypes.c_char_p, _IP, _IP, _IP, _I, _IP, ctypes.c_int64, _I64P]),
+    "s2_schedule_validate": (_I, [_SCH]),
+    "s2_schedule_to_json": (_I, [_SCH, ctypes.c_char_p, ctypes.c_size_t, _SZP]),
+    "s2_schedule_from_json": (_I, [ctypes.c_char_p, _CFG, _SCH, _IP, _I, _IP, _I]),
+    "s2_config_file_load": (_I, [ctypes.c_char_p, ctypes.POINTER(s2_config_file), _IP, _I, _IP, _I]),
+    "s2_equivalent_context_length": (_I, [ctypes.c_double] * 3 + [_DP]),
+    "s2_analytic_flops_reduction": (_I, [ctypes.c_double] * 3 + [_DP]),
+    "s2_speedup_upper_bound": (_I, [_I, ctypes.c_double, ctypes.c_double, _DP]),
+    "s2_exact_flops": (_I, [_CFG, _I, ctypes.POINTER(s2_flops_report), _I64P]),
+    "s2_simulate_decode_cache": (_I, [_CFG, _I, _I, _IP, _I64P, _IP, _I64P, _DP]),
+    "s2_kv_reduction": (_I, [_SCH, _DP]),
     "s2_profile_enable": (_I, [_I]),
     "s2_profile_collect": (_I, [_I, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), _IP, _IP]),
 }
@@ -129,6 +166,10 @@ class S2InvalidArgument(S2Error, ValueError):
 
 class S2Unsupported(S2Error, NotImplementedError):
     pass
+
+
+class S2ConfigError(S2Error):
+    """Maps load_config_file's std::runtime_error (serialize.cpp:123-146)."""
 
 
 _lib = None
@@ -158,4 +199,6 @@ def check(rc):
         raise S2InvalidArgument(rc, msg)
     if rc == S2_ERR_UNSUPPORTED:
         raise S2Unsupported(rc, msg)
+    if rc == S2_ERR_CONFIG:
+        raise S2ConfigError(rc, msg)
     raise S2Error(rc, msg)
