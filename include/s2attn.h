@@ -333,6 +333,22 @@ int s2_simulate_decode_cache(const s2_pattern_config* cfg, int total_tokens, int
  * averaged over heads and layers (dense layers keep everything). */
 int s2_kv_reduction(const s2_layer_schedule* schedule, double* percent);
 
+/* ---- hybrid layer stacks (reference LayerSchedule / build_layer_masks) ----
+ * One plan per distinct layer type of a schedule: the sparse pattern for S2
+ * layers and make_dense_config of the same shape (== dense_causal_mask,
+ * pattern.cpp:168-181,233-236) for the dense layer ids; every layer of a
+ * 24-layer model then runs through the same kernels with its own layout. */
+typedef struct s2_layers s2_layers;
+int s2_layers_create(const s2_layer_schedule* schedule, s2_layers** layers);
+void s2_layers_destroy(s2_layers* layers);
+/* Borrowed plan of `layer` (valid until s2_layers_destroy); *is_dense set when
+ * it is one of the dense layer ids. */
+int s2_layers_plan(s2_layers* layers, int layer, s2_plan** plan, int* is_dense);
+/* s2_attn_fwd / s2_attn_bwd with the layer's plan. */
+int s2_layers_fwd(s2_layers* layers, int layer, const s2_attn_args* args, s2_stream_t stream);
+int s2_layers_bwd(s2_layers* layers, int layer, const s2_attn_bwd_args* args, void* workspace,
+                  size_t workspace_bytes, s2_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,3 +18,4 @@ from .analysis import (  # noqa: F401
     CacheSchedule, FlopsReport, HeadCacheSchedule, analytic_flops_reduction,
     equivalent_context_length, exact_flops, flops_per_block_pair, kv_reduction,
     simulate_decode_cache, speedup_upper_bound)
+from .layers import LayerStack  # noqa: F401

@@ -149,6 +149,11 @@ SIGNATURES = {
     "s2_exact_flops": (_I, [_CFG, _I, ctypes.POINTER(s2_flops_report), _I64P]),
     "s2_simulate_decode_cache": (_I, [_CFG, _I, _I, _IP, _I64P, _IP, _I64P, _DP]),
     "s2_kv_reduction": (_I, [_SCH, _DP]),
+    "s2_layers_create": (_I, [_SCH, ctypes.POINTER(_P)]),
+    "s2_layers_destroy": (None, [_P]),
+    "s2_layers_plan": (_I, [_P, _I, ctypes.POINTER(_P), _IP]),
+    "s2_layers_fwd": (_I, [_P, _I, ctypes.POINTER(s2_attn_args), _P]),
+    "s2_layers_bwd": (_I, [_P, _I, ctypes.POINTER(s2_attn_bwd_args), _P, ctypes.c_size_t, _P]),
     "s2_profile_enable": (_I, [_I]),
     "s2_profile_collect": (_I, [_I, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), _IP, _IP]),
 }

@@ -93,3 +93,32 @@ def test_autograd_op():
     torch.testing.assert_close(o.float(), of, rtol=2e-2, atol=2e-2)
     for a, b in ((q, qf), (k, kf), (v, vf)):
         torch.testing.assert_close(a.grad.float(), b.grad, rtol=5e-2, atol=5e-2)
+
+
+def test_hybrid_layer_stack_fwd_bwd():
+    """A 4-layer hybrid stack (dense {0, 2}): each layer's fwd+bwd through
+    LayerStack equals the oracle on that layer's layout (build_layer_masks)."""
+    import torch
+
+    from paper_2407_17678_b200.pattern import LayerSchedule
+
+    pat = single(1024, 64, 4, 2, 3)
+    sched = LayerSchedule(4, {0, 2}, pat)
+    stack = s2.LayerStack(sched)
+    H, N, D = 4, 1024, 128
+    rng = np.random.default_rng(3)
+    dev = torch.device("cuda")
+    for layer in range(4):
+        cfg = s2.make_dense_config(N, 64, H) if layer in (0, 2) else pat
+        x = [bf16_round(rng.uniform(-1, 1, H * N * D).astype(np.float32)) for _ in range(4)]
+        tq, tk, tv, tdo = (torch.from_numpy(a).reshape(1, H, N, D).to(dev, torch.bfloat16) for a in x)
+        out, lse = stack.forward(layer, tq, tk, tv)
+        dq, dk, dv = stack.backward(layer, tq, tk, tv, out, lse, tdo)
+        torch.cuda.synchronize()
+        rp, ci = oracle.csr_all(cfg)
+        ro, rl = oracle.attn_fwd(*x[:3], rp, ci, 1, H, H, N, D, 64)
+        rq, rk, rv = oracle.attn_bwd(*x, rp, ci, 1, H, H, N, D, 64)
+        f = lambda t: t.float().cpu().numpy().ravel()  # noqa: E731
+        np.testing.assert_allclose(f(out), ro, **TOL)
+        for g, r in ((dq, rq), (dk, rk), (dv, rv)):
+            np.testing.assert_allclose(f(g), r, **TOL)
