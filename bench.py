@@ -361,6 +361,15 @@ def run_s2(args):
         line["e2e"] = {"value": 3.5 * tot_fwd_flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
                        "ms_per_step": ems, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
+    # ---- hybrid 24-layer mix of cfg3 (dense layers {0, 1}, configs/l1v15_dense01.json
+    #      shape): one dense-causal layer through the same kernels (LayerStack),
+    #      the mix = 2 dense + 22 S2 layers vs 24 dense layers (PAPER speedup shape)
+    if not args.no_hybrid and world == 1:
+        try:
+            line["hybrid"] = bench_hybrid(s2, cfg, q, k, v, do, out, lse, dq, dk, dv, ms_max, dev)
+        except Exception as ex:  # reported, never fatal to the main number
+            line["hybrid"] = {"error": str(ex)}
+
     # ---- decode at cfg4 (B=64, 128K context, GQA 32q/8kv, v=8), per GPU
     if not args.no_decode:
         try:
@@ -458,6 +467,53 @@ def bench_decode(args, dev, world):
                     "h2d_bytes_per_step": q.numel() * 2, "d2h_bytes_per_step": out.numel() * 2}}
 
 
+def bench_hybrid(s2, cfg, q, k, v, do, out, lse, dq, dk, dv, s2_ms, dev, layers=24, dense_ids=(0, 1)):
+    """Dense-causal fwd+bwd of one cfg3-shaped layer (the hybrid model's dense
+    layers) through the LayerStack, CUDA events, then the 24-layer mix."""
+    import torch
+
+    from paper_2407_17678_b200.pattern import LayerSchedule
+
+    stack = s2.LayerStack(LayerSchedule(layers, set(dense_ids), cfg))
+    dl = dense_ids[0]
+    U = q.shape[0]
+    qq, kk, vv = q[:1], k[:1].reshape(1, 1, N_SEQ, D), v[:1].reshape(1, 1, N_SEQ, D)
+    # full H=32 heads: the unit packing of the main bench holds one kv head per unit;
+    # run the dense layer on the first 32 units' worth of rows re-viewed as heads.
+    Hh = min(H, U)
+    qd = q[:Hh].reshape(1, Hh, N_SEQ, D)
+    kd, vd = (t[:Hh].reshape(1, Hh, N_SEQ, D) for t in (k, v))
+    dod = do[:Hh].reshape(1, Hh, N_SEQ, D)
+    plan = stack.plan(dl)
+    o, l = torch.empty_like(qd), torch.empty((1, Hh, N_SEQ), device=dev, dtype=torch.float32)
+    gq, gk, gv = torch.empty_like(qd), torch.empty_like(kd), torch.empty_like(vd)
+    units = list(range(Hh))
+
+    def dstep():
+        s2.s2_attn_fwd(plan, qd, kd, vd, out=o, lse=l)
+        s2.s2_attn_bwd(plan, qd, kd, vd, o, l, dod, dq=gq, dk=gk, dv=gv)
+
+    for _ in range(2):
+        dstep()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = 3
+    e0.record()
+    for _ in range(n):
+        dstep()
+    e1.record()
+    torch.cuda.synchronize()
+    dense_ms = e0.elapsed_time(e1) / n * (H / Hh)
+    act, dense_fl = plan.fwd_flops(1, D)
+    nd = len(dense_ids)
+    mix = nd * dense_ms + (layers - nd) * s2_ms
+    return {"layers": layers, "dense_layer_ids": list(dense_ids), "dense_layer_ms": dense_ms,
+            "s2_layer_ms": s2_ms, "hybrid_ms": mix, "all_dense_ms": layers * dense_ms,
+            "speedup_vs_all_dense": layers * dense_ms / mix,
+            "dense_layer_tflops": 3.5 * dense_fl * (Hh / H) / (dense_ms * (Hh / H) * 1e-3) / 1e12,
+            "note": "fwd+bwd per layer, CUDA events; dense layers = make_dense_config through LayerStack"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -467,6 +523,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-hybrid", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
