@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 
 N_SEQ, H, D, BLOCK, LOCAL, VSTRIDE = 32768, 32, 128, 64, 4, 16
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+COMM_SMS = 16  # SMs left to NCCL when N > 1
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -232,7 +233,11 @@ def run_s2(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's all-gather CTAs share the GPU with the backward: cap them and
+        # keep their SMs out of the persistent kernels' grid (s2_set_sm_reserve)
+        os.environ.setdefault("NCCL_MAX_CTAS", str(COMM_SMS))
         dist.init_process_group("nccl", device_id=dev)
+        _abi.check(_abi.lib().s2_set_sm_reserve(int(os.environ["NCCL_MAX_CTAS"])))
     cfg = workload_cfg()
     plan = s2.Plan.from_config(cfg)
     hp = HeadParallelPlan(plan, world, world)  # global batch = world (weak scaling)
@@ -255,9 +260,11 @@ def run_s2(args):
 
     def step():
         s2.s2_attn_fwd(plan, q, k, v, out=out, lse=lse, unit_ids=units)
-        if world > 1:
-            hp.all_gather(out.reshape(U, 1, N_SEQ, D))
+        finish = hp.all_gather_async(out.reshape(U, 1, N_SEQ, D)) if world > 1 else None
+        # the backward needs only this rank's units: it overlaps the all-gather
         s2.s2_attn_bwd(plan, q, k, v, out, lse, do, dq=dq, dk=dk, dv=dv, unit_ids=units)
+        if finish is not None:
+            finish()
 
     def barrier():
         if world > 1:

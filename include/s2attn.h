@@ -52,6 +52,11 @@ enum {
     S2_ERR_BUFFER_TOO_SMALL = 7
 };
 
+/* SMs the persistent tcgen05 kernels leave free for concurrent work (e.g.
+ * NCCL's all-gather CTAs on a communication stream overlapping the
+ * backward): their grid becomes (SM count - sms).  Process-wide; 0 default. */
+int s2_set_sm_reserve(int sms);
+
 /* Message for the last non-zero status returned on this thread. */
 const char* s2_last_error(void);
 int s2_abi_version(void);

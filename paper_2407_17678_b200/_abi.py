@@ -91,6 +91,7 @@ _DP = ctypes.POINTER(ctypes.c_double)
 SIGNATURES = {
     "s2_last_error": (ctypes.c_char_p, []),
     "s2_abi_version": (_I, []),
+    "s2_set_sm_reserve": (_I, [_I]),
     "s2_make_single_stride_config": (_I, [_I, _I, _I, _I, _I, _I, _CFG]),
     "s2_pattern_validate": (_I, [_CFG]),
     "s2_pattern_num_blocks": (_I, [_CFG]),

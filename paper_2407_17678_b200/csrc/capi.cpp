@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -177,7 +178,8 @@ static int dkv_group() {
 // ui-th listed unit is ui*hpg + j (= b*H + h when every unit is listed).
 WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* unit_ids,
                      int* status) {
-    std::string key = std::to_string(batch) + ":";
+    const int grid = persistent_grid();
+    std::string key = std::to_string(batch) + ":g" + std::to_string(grid) + ":";
     std::vector<int> units;
     if (unit_ids) {
         units.assign(unit_ids, unit_ids + num_units);
@@ -220,7 +222,6 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
                 const int cnt = static_cast<int>(L->fwd.offset[w_ + 1] - off);
                 fi.push_back({bh[i], head[i], t, cnt, off});
             }
-        const int grid = num_sms();
         const std::vector<int32_t> off_fwd = schedule_items(
             fi, grid, [](const s2dev::FwdItem& a) { return int64_t(a.chunk_cnt); },
             [](const s2dev::FwdItem& a) { return a.bh; }, 2);
@@ -325,6 +326,13 @@ int num_sms() {
     return n;
 }
 
+static std::atomic<int> g_sm_reserve{0};
+
+// CTAs of the persistent tcgen05 kernels: one per SM minus the SMs left to
+// concurrent work (NCCL's all-gather CTAs on a communication stream), so a
+// static schedule never waits for an SM that a collective occupies.
+int persistent_grid() { return std::max(1, num_sms() - g_sm_reserve.load()); }
+
 bool use_tcgen05(const s2_plan* p, const s2_attn_args* a) {
     return a->dtype == S2_DTYPE_BF16 && p->block_size % 16 == 0 &&
            (a->head_dim == 64 || a->head_dim == 128);
@@ -354,6 +362,12 @@ using namespace s2;
 extern "C" {
 
 const char* s2_last_error(void) { return g_last_error.c_str(); }
+
+int s2_set_sm_reserve(int sms) {
+    if (sms < 0) return fail(S2_ERR_INVALID_ARGUMENT, "sm reserve must be >= 0");
+    g_sm_reserve.store(sms);
+    return S2_OK;
+}
 int s2_abi_version(void) { return S2_ABI_VERSION; }
 
 int s2_make_single_stride_config(int seq_len, int block_size, int num_heads, int local_blocks,

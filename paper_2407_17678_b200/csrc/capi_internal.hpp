@@ -13,6 +13,7 @@ int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 int check_args(const s2_plan* p, const s2_attn_args* a);
 int num_sms();
+int persistent_grid();  // num_sms() minus s2_set_sm_reserve
 bool use_tcgen05(const s2_plan* p, const s2_attn_args* a);
 int ensure_csr_uploaded(s2_plan* p);
 Lists* get_lists(s2_plan* p, int seq_len, int* status);

@@ -75,6 +75,17 @@ class HeadParallelPlan:
 
         One all_gather of equal-sized (max-unit padded) buffers; no other
         collective on the data path."""
+        return self.all_gather_async(local, group)()
+
+    def all_gather_async(self, local, group=None):
+        """Start the all-gather and return finish() -> full tensor.
+
+        The collective runs on the communication stream of the process group
+        (NCCL's own stream), so work issued between start and finish — the
+        backward, which needs only this rank's output and lse — overlaps the
+        NVLink transfer.  finish() makes the current stream wait and unpacks.
+        Pair with s2_set_sm_reserve so the persistent kernels leave NCCL's CTAs
+        their SMs."""
         import torch
         import torch.distributed as dist
 
@@ -83,14 +94,19 @@ class HeadParallelPlan:
                           device=local.device)
         pad[:U] = local
         bufs = [torch.empty_like(pad) for _ in range(self.world_size)]
-        dist.all_gather(bufs, pad, group=group)
-        full = torch.empty((self.batch * self.plan.num_kv_heads,) + tuple(local.shape[1:]),
-                           dtype=local.dtype, device=local.device)
-        for r in range(self.world_size):
-            n = len(self.units[r])
-            if n:
-                full[self._index(r, local.device)] = bufs[r][:n]
-        return full
+        work = dist.all_gather(bufs, pad, group=group, async_op=True)
+
+        def finish():
+            work.wait()
+            full = torch.empty((self.batch * self.plan.num_kv_heads,) + tuple(local.shape[1:]),
+                               dtype=local.dtype, device=local.device)
+            for r in range(self.world_size):
+                n = len(self.units[r])
+                if n:
+                    full[self._index(r, local.device)] = bufs[r][:n]
+            return full
+
+        return finish
 
 
 def head_parallel_forward(plan, q, k, v, rank: int, world_size: int, *, group=None,

@@ -71,6 +71,14 @@ def _worker(rank, world, port, cfg, batch, D, res_path):
     hp = HeadParallelPlan(plan, batch, world)
     out, lse = head_parallel_forward(plan, q, k, v, rank, world, hp=hp,
                                      local_fn=_oracle_local(cfg))
+    # bench.py's overlapped form: start the gather, do unrelated local work (the
+    # backward there), finish: the same bytes
+    ql = hp.scatter_q(q, rank)
+    finish = hp.all_gather_async(ql)
+    _ = (ql * 2).sum()  # work between start and finish
+    gathered = finish()
+    B_, H_, N_, D_ = q.shape
+    assert torch.equal(gathered.reshape(B_, H_, N_, D_), q)
     if rank == 0:
         np.savez(res_path, out=out.numpy(), lse=lse.numpy(), q=q.numpy(), k=k.numpy(),
                  v=v.numpy(), load=hp.load, owner=hp.owner)
