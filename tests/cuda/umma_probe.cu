@@ -568,3 +568,53 @@ extern "C" int probe_dkv2(int steps, int variant, long long* host_out) {
     cudaFree(d);
     return e == cudaSuccess ? 0 : 2;
 }
+
+// ---- TMEM load bandwidth: `nw` warps each issue `iters` x (4 x tcgen05.ld.32x32b.x32)
+// then wait; reports cycles of the slowest warp.
+__global__ void __launch_bounds__(512, 1) probe_tmem_ld_kernel(int nw, int iters, long long* out) {
+    __shared__ uint32_t tmem_base_s;
+    __shared__ unsigned long long tmax;
+    const int tid = threadIdx.x, warp = tid / 32;
+    if (warp == 0) {
+        tmem_alloc(smem_u32(&tmem_base_s), 512);
+        tmem_relinquish();
+    }
+    if (tid == 0) tmax = 0;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = tmem_base_s;
+    if (warp < nw) {
+        const uint32_t lo = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        uint32_t acc = 0;
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            uint32_t r0[32], r1[32], r2[32], r3[32];
+            const uint32_t col = ((warp >> 2) * 128 + (i & 1) * 0) & 511;
+            tmem_ld32(tb + lo + col, r0);
+            tmem_ld32(tb + lo + col + 32, r1);
+            tmem_ld32(tb + lo + col + 64, r2);
+            tmem_ld32(tb + lo + col + 96, r3);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc += r0[j] ^ r1[j] ^ r2[j] ^ r3[j];
+        }
+        const long long t1 = clock64();
+        if ((tid & 31) == 0) atomicMax(&tmax, static_cast<unsigned long long>(t1 - t0));
+        if (acc == 0x12345678u) out[1] = acc;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) out[0] = static_cast<long long>(tmax);
+    if (warp == 0) tmem_dealloc(tb, 512);
+}
+
+extern "C" int probe_tmem_ld(int nw, int iters, long long* host_out) {
+    long long* d;
+    cudaMalloc(&d, 16);
+    probe_tmem_ld_kernel<<<1, 512>>>(nw, iters, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(host_out, d, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? 0 : 2;
+}

@@ -28,3 +28,8 @@ for m, name in enumerate(modes):
 for v, name in ((1, "S,dP"), (2, "dV,dK"), (3, "all"), (7, "all + TMEM ld/st"), (11, "all + TMA"), (15, "all + TMEM + TMA")):
     assert L.probe_dkv2(512, v, out) == 0
     print(f"dkv2 [{name}]: {out[0]/512:.0f} cyc/step (ideal S,dP 512 + dV,dK 512)")
+for nw in (1, 4, 8, 16):
+    it = 256
+    assert L.probe_tmem_ld(nw, it, out) == 0
+    by = nw * it * 4 * 32 * 32 * 4
+    print(f"tmem ld: {nw:2d} warps: {out[0]/it:7.1f} cyc per 4 x x32 per warp; {by/out[0]:6.1f} B/cycle/SM")

@@ -15,12 +15,12 @@ plan = s2.Plan.from_config(s2.make_s2_config(32768, 32, local_blocks=4, vert_str
 mk = lambda: torch.randn(1, 32, 32768, 128, device="cuda", dtype=torch.bfloat16)  # noqa
 q, k, v = mk(), mk(), mk()
 out, lse = s2.s2_attn_fwd(plan, q, k, v)
-tr = torch.zeros(8 * 2048, dtype=torch.int64, device="cuda")
+tr = torch.zeros(16 * 2048, dtype=torch.int64, device="cuda")
 L.s2_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
 s2.s2_attn_fwd(plan, q, k, v, out=out, lse=lse)
 torch.cuda.synchronize()
 L.s2_debug_set_trace(None)
-t = tr.cpu().numpy().reshape(8, 2048).astype(np.int64)
+t = tr.cpu().numpy().reshape(16, 2048).astype(np.int64)
 n = int((t[5] > 0).sum())
 m = lambda a: float(np.median(a))  # noqa
 lo, hi = 20, min(n, 1500)
@@ -29,3 +29,11 @@ print("softmax0: wait S", m(t[5, lo:hi] - t[4, lo:hi]), " step period", m(np.dif
 print("softmax0: S ok -> next wait (compute+store+arrive)", m(t[4, lo + 1:hi + 1] - t[5, lo:hi]))
 print("softmax1: wait S", m(t[7, lo:hi] - t[6, lo:hi]), " compute", m(t[6, lo + 1:hi + 1] - t[7, lo:hi]))
 print("MMA: wait P0", m(t[1, lo:hi] - t[0, lo:hi]), " wait K", m(t[3, lo:hi] - t[2, lo:hi]))
+if (t[12] > 0).sum() > 10:  # built with -DS2_FWD_DETAIL_TRACE
+    k = np.arange(lo, hi)
+    names = ["S ok -> ld done", "mask + local max", "max exchange", "exp + P store", "rescale + st wait + arrive"]
+    prev = t[5, k - 1]  # slot 5 uses the pre-increment count
+    for i, nm in enumerate(names):
+        cur = t[8 + i, k]
+        print(f"  {nm}: {np.median(cur - prev):.0f}")
+        prev = cur
