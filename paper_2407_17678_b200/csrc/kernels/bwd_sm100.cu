@@ -83,16 +83,18 @@ struct BwdCfg {
     static constexpr int kTile128 = kSub * 16384;  // 128 rows x D bf16
     static constexpr int kTile64 = kSub * 8192;    // 64 rows x D bf16
     // dkv: resident K, V (128 keys); kNSTkv stages of Q64, dO64 (1024-B aligned
-    // SW128 tiles); an aux slot per stage (lse2[64], delta[64], meta); the
-    // epilogue's staging tiles for the TMA stores of dV and dK (2 x 128 x D bf16).
+    // SW128 tiles); an aux slot per stage (lse2[64], delta[64], meta).
+    // The resident operands are double-buffered across items (the next
+    // item's load runs under this one) and a finished item's dead buffer is
+    // the staging tile of its epilogue's TMA stores.
     static constexpr int kNSTkv = 3;
     static constexpr int kDkvStage = 2 * kTile64;
     static constexpr int kAux = 528;
-    static constexpr int kDkvSmem = 1024 + 2 * kTile128 + kNSTkv * kDkvStage + 2 * kTile128 + kNSTkv * kAux;
-    // dq: resident Q, dO (128 rows); kNSTq stages of K64, V64; staging for dQ (128 x D)
-    static constexpr int kNSTq = 4;
+    static constexpr int kDkvSmem = 1024 + 4 * kTile128 + kNSTkv * kDkvStage + kNSTkv * kAux;
+    // dq: resident Q, dO (128 rows) double-buffered; kNSTq stages of K64, V64
+    static constexpr int kNSTq = 3;
     static constexpr int kDqStage = 2 * kTile64;
-    static constexpr int kDqSmem = 1024 + 2 * kTile128 + kNSTq * kDqStage + kTile128;
+    static constexpr int kDqSmem = 1024 + 4 * kTile128 + kNSTq * kDqStage;
 };
 
 // Stage layout of the dK/dV kernel: Q rows [64][D] | dO rows [64][D] |
@@ -113,20 +115,24 @@ __global__ void __launch_bounds__(384, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_kvf, bar_kve, bar_sf[NST], bar_se[NST], bar_s[2], bar_p[2], bar_af, bar_ae;
+    // bar_kve[kb]: K/V buffer kb is free (its item's last S^T/dP^T MMAs done AND both
+    // epilogue TMA stores, staged in it, have read it): count 3
+    __shared__ uint64_t bar_kvf[2], bar_kve[2], bar_sf[NST], bar_se[NST], bar_s[2], bar_p[2], bar_af, bar_ae;
     __shared__ uint32_t tmem_base_s;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // K/V buffer kb: K at sK + kb * 2 * kTile128, V right after it
     const uint32_t sK = smem_u32(smem), sV = sK + C::kTile128;
-    const uint32_t sSt = sV + C::kTile128;
-    const uint32_t sOut = sSt + NST * C::kDkvStage;  // [wg: dV, dK][chunk][D/64][64 rows][128 B]
-    const uint32_t sAux = sOut + 2 * C::kTile128;
+    const uint32_t sSt = sK + 4 * C::kTile128;
+    const uint32_t sAux = sSt + NST * C::kDkvStage;
     uint8_t* const gAux = smem + (sAux - sK);  // generic pointer to aux 0
     const BwdItem* items = static_cast<const BwdItem*>(p.items);
     const BwdEntry* ents = static_cast<const BwdEntry*>(p.entries);
 
     if (tid == 0) {
-        mbar_init(smem_u32(&bar_kvf), 1);
-        mbar_init(smem_u32(&bar_kve), 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&bar_kvf[i]), 1);
+            mbar_init(smem_u32(&bar_kve[i]), 3);
+        }
         mbar_init(smem_u32(&bar_af), 1);
         mbar_init(smem_u32(&bar_ae), 256);
         for (int i = 0; i < NST; ++i) {
@@ -161,15 +167,16 @@ __global__ void __launch_bounds__(384, 1)
             uint32_t it_cnt = 0, st_it = 0;
             for (int i = i_beg; i < i_end; ++i, ++it_cnt) {
                 const BwdItem it = items[i];
-                if (it_cnt > 0) mbar_wait(smem_u32(&bar_kve), (it_cnt - 1) & 1);
+                const int kb = it_cnt & 1;
+                if (it_cnt >= 2) mbar_wait(smem_u32(&bar_kve[kb]), ((it_cnt >> 1) - 1) & 1);
                 const int nc = it.c1 >= 0 ? 2 : 1;
-                const uint32_t kvbar = smem_u32(&bar_kvf);
+                const uint32_t kvbar = smem_u32(&bar_kvf[kb]), kvoff = kb * 2 * C::kTile128;
                 mbar_expect_tx(kvbar, 2 * nc * C::kSub * 8192);
                 for (int h = 0; h < nc; ++h)
                     for (int s = 0; s < C::kSub; ++s) {
                         const int row = (h ? it.c1 : it.c0) * 64;
-                        tma_load_3d(sK + s * 16384 + h * 8192, &tmK, kvbar, s * 64, row, it.kvbh);
-                        tma_load_3d(sV + s * 16384 + h * 8192, &tmV, kvbar, s * 64, row, it.kvbh);
+                        tma_load_3d(sK + kvoff + s * 16384 + h * 8192, &tmK, kvbar, s * 64, row, it.kvbh);
+                        tma_load_3d(sV + kvoff + s * 16384 + h * 8192, &tmV, kvbar, s * 64, row, it.kvbh);
                     }
                 for (int j = 0; j < p.hpg; ++j) {
                     const int qbh = it.kvbh * p.hpg + j;
@@ -215,7 +222,9 @@ __global__ void __launch_bounds__(384, 1)
             uint32_t it_cnt = 0, st_it = 0;
             for (int i = i_beg; i < i_end; ++i, ++it_cnt) {
                 const int nsteps = warp_uniform(items[i].nsteps);
-                mbar_wait(smem_u32(&bar_kvf), it_cnt & 1);
+                const int kb = it_cnt & 1;
+                const uint32_t kvoff = (kb * 2 * C::kTile128) >> 4;
+                mbar_wait(smem_u32(&bar_kvf[kb]), (it_cnt >> 1) & 1);
                 auto accumulate = [&](uint32_t n, int st, bool first) {
                     const int b = n & 1;
                     S2TRACE(3, n);
@@ -256,14 +265,15 @@ __global__ void __launch_bounds__(384, 1)
                             const uint32_t ao = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
                             const uint32_t bo = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
                             // S^T = K Q^T ; dP^T = V dO^T  (K-major x K-major)
-                            mma_ss(tmem + b * 64, dK0 + ao, dst + bo, idS, kk > 0);
-                            mma_ss(tmem + 128 + b * 64, dV0 + ao, dst + ((C::kTile64 >> 4) + bo), idS, kk > 0);
+                            mma_ss(tmem + b * 64, dK0 + kvoff + ao, dst + bo, idS, kk > 0);
+                            mma_ss(tmem + 128 + b * 64, dV0 + kvoff + ao, dst + ((C::kTile64 >> 4) + bo), idS,
+                                   kk > 0);
                         }
                         mma_commit(smem_u32(&bar_s[b]));
                         // K / V are read by the S^T / dP^T MMAs only: release them after
                         // the item's last ones so the next item's K / V load overlaps the
                         // last dV / dK update and the epilogue.
-                        if (s == nsteps - 1) mma_commit(smem_u32(&bar_kve));
+                        if (s == nsteps - 1) mma_commit(smem_u32(&bar_kve[kb]));
                     }
                     __syncwarp();
                     S2TRACE(2, n);
@@ -285,6 +295,7 @@ __global__ void __launch_bounds__(384, 1)
         const int cg = (kr & 63) >> 4;
         const int hk = kr >> 6;
         uint32_t it_cnt = 0, st_it = 0;
+        int release = -1;  // WG leader: K/V buffer whose epilogue store is still in flight
         for (int i = i_beg; i < i_end; ++i, ++it_cnt) {
             const BwdItem it = items[i];
             const int chunk = hk ? it.c1 : it.c0;
@@ -359,6 +370,11 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_before();
                 mbar_arrive(smem_u32(&bar_p[b]));
                 if (tid == 128) S2TRACE(7, st_it);
+                if (release >= 0) {  // the previous item's store read its staging long ago
+                    bulk_wait_read0();
+                    mbar_arrive(smem_u32(&bar_kve[release]));
+                    release = -1;
+                }
             }
             // ---------------------------------------------------- epilogue
             // TMEM -> registers (then the accumulators are released), bf16 into
@@ -377,8 +393,14 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_before();
             mbar_arrive(smem_u32(&bar_ae));
             const bool wg_leader = (tid & 127) == 0;
-            if (wg_leader) bulk_wait_read0();  // previous item's stores have read the staging tile
-            named_bar_sync(1 + wg, 128);
+            if (release >= 0) {  // (an item without steps: release here at the latest)
+                bulk_wait_read0();
+                mbar_arrive(smem_u32(&bar_kve[release]));
+                release = -1;
+            }
+            // bar_af: every MMA of the item is done, so its K/V buffer is dead: stage dV
+            // over its K tile (wg 0) and dK over its V tile (wg 1)
+            const uint32_t sOut = sK + (it_cnt & 1) * 2 * C::kTile128;
             const uint32_t so = sOut + wg * C::kTile128 + hk * (C::kSub * 8192) + (kr & 63) * 128;
 #pragma unroll
             for (int c = 0; c < D / 8; ++c) {  // 16-byte chunk c of the row: D/64 slice c>>3
@@ -401,10 +423,12 @@ __global__ void __launch_bounds__(384, 1)
                                      ch * 64, it.kvbh);
                 }
                 bulk_commit();
+                release = static_cast<int>(it_cnt & 1);  // arrive on bar_kve once the store has read it
             }
             if (tid == 128) S2TRACE(10, it_cnt);
         }
         if ((tid & 127) == 0) bulk_wait0();  // staging tiles must outlive the stores
+        (void)release;
     }
     tc_fence_before();
     __syncthreads();
@@ -425,18 +449,22 @@ __global__ void __launch_bounds__(384, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_qf, bar_qe, bar_sf[NST], bar_se[NST], bar_s[2], bar_p[2], bar_af, bar_ae;
+    // bar_qe[qb]: Q/dO buffer qb is free (last S/dP MMAs done AND the dQ TMA store,
+    // staged in its Q tile, has read it): count 2
+    __shared__ uint64_t bar_qf[2], bar_qe[2], bar_sf[NST], bar_se[NST], bar_s[2], bar_p[2], bar_af, bar_ae;
     __shared__ uint32_t tmem_base_s;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // Q/dO buffer qb: Q at sQ + qb * 2 * kTile128, dO right after it
     const uint32_t sQ = smem_u32(smem), sdO = sQ + C::kTile128;
-    const uint32_t sSt = sdO + C::kTile128;
-    const uint32_t sOut = sSt + NST * C::kDqStage;  // dQ staging [D/64][128 rows][128 B]
+    const uint32_t sSt = sQ + 4 * C::kTile128;
     const FwdItem* items = static_cast<const FwdItem*>(p.items);
     const int2* chunks = static_cast<const int2*>(p.entries);
 
     if (tid == 0) {
-        mbar_init(smem_u32(&bar_qf), 1);
-        mbar_init(smem_u32(&bar_qe), 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&bar_qf[i]), 1);
+            mbar_init(smem_u32(&bar_qe[i]), 2);
+        }
         mbar_init(smem_u32(&bar_af), 1);
         mbar_init(smem_u32(&bar_ae), 256);
         for (int i = 0; i < NST; ++i) {
@@ -471,12 +499,13 @@ __global__ void __launch_bounds__(384, 1)
             for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
                 const FwdItem it = items[i];
                 const int kvbh = it.bh / p.hpg;
-                if (it_cnt > 0) mbar_wait(smem_u32(&bar_qe), (it_cnt - 1) & 1);
-                const uint32_t qbar = smem_u32(&bar_qf);
+                const int qb = it_cnt & 1;
+                if (it_cnt >= 2) mbar_wait(smem_u32(&bar_qe[qb]), ((it_cnt >> 1) - 1) & 1);
+                const uint32_t qbar = smem_u32(&bar_qf[qb]), qoff = qb * 2 * C::kTile128;
                 mbar_expect_tx(qbar, 2 * C::kTile128);
                 for (int s = 0; s < C::kSub; ++s) {
-                    tma_load_3d(sQ + s * 16384, &tmQ, qbar, s * 64, it.qtile * 128, it.bh);
-                    tma_load_3d(sdO + s * 16384, &tmdO, qbar, s * 64, it.qtile * 128, it.bh);
+                    tma_load_3d(sQ + qoff + s * 16384, &tmQ, qbar, s * 64, it.qtile * 128, it.bh);
+                    tma_load_3d(sdO + qoff + s * 16384, &tmdO, qbar, s * 64, it.qtile * 128, it.bh);
                 }
                 for (int n = 0; n < it.chunk_cnt; ++n, ++st_it) {
                     const int st = st_it % NST;
@@ -503,7 +532,9 @@ __global__ void __launch_bounds__(384, 1)
             const int i_end = p.sched[blockIdx.x + 1];
             for (int i = p.sched[blockIdx.x]; i < i_end; ++i, ++it_cnt) {
                 const int chunk_cnt = warp_uniform(items[i].chunk_cnt);
-                mbar_wait(smem_u32(&bar_qf), it_cnt & 1);
+                const int qb = it_cnt & 1;
+                const uint32_t qoff = (qb * 2 * C::kTile128) >> 4;
+                mbar_wait(smem_u32(&bar_qf[qb]), (it_cnt >> 1) & 1);
                 bool first = true;
                 auto accumulate = [&](uint32_t n, int st) {
                     const int b = n & 1;
@@ -537,12 +568,13 @@ __global__ void __launch_bounds__(384, 1)
                         for (int kk = 0; kk < D / 16; ++kk) {
                             const uint32_t ao = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
                             const uint32_t bo = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
-                            mma_ss(tmem + b * 64, dQ0 + ao, dst + bo, idS, kk > 0);
-                            mma_ss(tmem + 128 + b * 64, ddO0 + ao, dst + ((C::kTile64 >> 4) + bo), idS, kk > 0);
+                            mma_ss(tmem + b * 64, dQ0 + qoff + ao, dst + bo, idS, kk > 0);
+                            mma_ss(tmem + 128 + b * 64, ddO0 + qoff + ao, dst + ((C::kTile64 >> 4) + bo), idS,
+                                   kk > 0);
                         }
                         mma_commit(smem_u32(&bar_s[b]));
                         // Q / dO feed only S / dP: release them after the item's last ones
-                        if (n == chunk_cnt - 1) mma_commit(smem_u32(&bar_qe));
+                        if (n == chunk_cnt - 1) mma_commit(smem_u32(&bar_qe[qb]));
                     }
                     __syncwarp();
                     S2TRACE(2, n_glob);
@@ -552,7 +584,7 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 if (prev_st >= 0) accumulate(prev_n, prev_st);
                 if (leader) {
-                    if (chunk_cnt == 0) mma_commit(smem_u32(&bar_qe));  // (user CSR with empty rows)
+                    if (chunk_cnt == 0) mma_commit(smem_u32(&bar_qe[qb]));  // (user CSR with empty rows)
                     mma_commit(smem_u32(&bar_af));
                 }
                 __syncwarp();
@@ -565,6 +597,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const float sl2 = p.scale_log2;
         uint32_t it_cnt = 0, n_glob = 0;
+        int release = -1;  // leader: Q/dO buffer whose dQ store is still in flight
         for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
             const FwdItem it = items[i];
             const int q_pos = it.qtile * 128 + r;
@@ -614,6 +647,11 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_before();
                 mbar_arrive(smem_u32(&bar_p[b]));
                 if (tid == 128) S2TRACE(7, n_glob);
+                if (release >= 0) {  // the previous item's store read its staging long ago
+                    bulk_wait_read0();
+                    mbar_arrive(smem_u32(&bar_qe[release]));
+                    release = -1;
+                }
             }
             mbar_wait(smem_u32(&bar_af), it_cnt & 1);
             tc_fence_after();
@@ -627,8 +665,13 @@ __global__ void __launch_bounds__(384, 1)
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(smem_u32(&bar_ae));
-            if (tid == 128) bulk_wait_read0();  // previous item's store has read the staging tile
-            named_bar_sync(1, 256);
+            if (release >= 0) {  // (an item without chunks: release here at the latest)
+                bulk_wait_read0();
+                mbar_arrive(smem_u32(&bar_qe[release]));
+                release = -1;
+            }
+            // bar_af: every MMA of the item is done, so its Q tile is dead: stage dQ there
+            const uint32_t sOut = sQ + (it_cnt & 1) * 2 * C::kTile128;
             const float sc = it.chunk_cnt > 0 ? p.scale : 0.f;  // no chunks: dQ = 0
 #pragma unroll
             for (int c = 0; c < D / 16; ++c) {  // my 16-byte chunks: global chunk index g
@@ -646,9 +689,11 @@ __global__ void __launch_bounds__(384, 1)
                 for (int sb = 0; sb < C::kSub; ++sb)
                     tma_store_3d(&tmdQ, sOut + sb * 16384, sb * 64, it.qtile * 128, it.bh);
                 bulk_commit();
+                release = static_cast<int>(it_cnt & 1);  // arrive on bar_qe once the store has read it
             }
         }
         if (tid == 128) bulk_wait0();  // the staging tile must outlive the store
+        (void)release;
     }
     tc_fence_before();
     __syncthreads();
