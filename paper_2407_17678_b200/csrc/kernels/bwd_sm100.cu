@@ -21,39 +21,49 @@
 // the MMAs of steps n-1 and n+1.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "sm100_ptx.cuh"
 
 namespace s2dev {
 
 // ------------------------------------------------------------------ prep
+// Delta = rowsum(dO o O) and lse*log2(e) per row; HBM-bound (reads O and dO
+// once).  D/8 lanes own a row (16-byte loads), 256 / (D/8) rows per 256-thread
+// block iteration, grid-stride over rows.
+template <int D>
 __global__ void __launch_bounds__(256) s2_bwd_prep_kernel(const __nv_bfloat16* __restrict__ out,
                                                           const __nv_bfloat16* __restrict__ dout,
                                                           const float* __restrict__ lse,
                                                           float* __restrict__ delta,
                                                           float* __restrict__ lse2, int num_bh,
-                                                          int N, int Npad, int D) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+                                                          int N, int Npad) {
+    constexpr int LPR = D / 8;  // lanes per row
     const long long total = static_cast<long long>(num_bh) * Npad;
-    if (warp >= total) return;
-    const int bh = static_cast<int>(warp / Npad), row = static_cast<int>(warp % Npad);
-    float acc = 0.f;
-    if (row < N) {
-        const __nv_bfloat16* o = out + (static_cast<size_t>(bh) * N + row) * D;
-        const __nv_bfloat16* g = dout + (static_cast<size_t>(bh) * N + row) * D;
-        for (int x = lane * 2; x < D; x += 64) {
-            const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(o + x);
-            const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(g + x);
-            acc = fmaf(__low2float(a), __low2float(b), acc);
-            acc = fmaf(__high2float(a), __high2float(b), acc);
-        }
-    }
+    const int sub = threadIdx.x % LPR;
+    for (long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / LPR; row < total;
+         row += static_cast<long long>(gridDim.x) * blockDim.x / LPR) {
+        const int bh = static_cast<int>(row / Npad), t = static_cast<int>(row % Npad);
+        float acc = 0.f;
+        if (t < N) {
+            const size_t off = (static_cast<size_t>(bh) * N + t) * D + sub * 8;
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(out + off));
+            const uint4 b = __ldg(reinterpret_cast<const uint4*>(dout + off));
+            const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-    if (lane == 0) {
-        delta[warp] = acc;
-        lse2[warp] = row < N ? lse[static_cast<size_t>(bh) * N + row] * 1.4426950408889634f : INFINITY;
+            for (int j = 0; j < 4; ++j) {
+                const float2 x = __bfloat1622float2(a2[j]), y = __bfloat1622float2(b2[j]);
+                acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+            }
+        }
+#pragma unroll
+        for (int s = LPR / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+        if (sub == 0) {
+            delta[row] = acc;
+            lse2[row] = t < N ? lse[static_cast<size_t>(bh) * N + t] * 1.4426950408889634f : INFINITY;
+        }
     }
 }
 
@@ -717,9 +727,16 @@ long long* s2_debug_trace_buffer() { return g_trace; }
 cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* dout,
                                const float* lse, float* delta, float* lse2, int num_bh, int N,
                                int Npad, int D, cudaStream_t stream) {
-    const long long warps = static_cast<long long>(num_bh) * Npad;
-    const int blocks = static_cast<int>((warps * 32 + 255) / 256);
-    s2_bwd_prep_kernel<<<blocks, 256, 0, stream>>>(out, dout, lse, delta, lse2, num_bh, N, Npad, D);
+    const long long rows = static_cast<long long>(num_bh) * Npad;
+    const int per_block = 256 / (D / 8);
+    const long long need = (rows + per_block - 1) / per_block;
+    const int blocks = static_cast<int>(std::min<long long>(need, 148LL * 8));
+    if (D == 128)
+        s2_bwd_prep_kernel<128><<<blocks, 256, 0, stream>>>(out, dout, lse, delta, lse2, num_bh, N, Npad);
+    else if (D == 64)
+        s2_bwd_prep_kernel<64><<<blocks, 256, 0, stream>>>(out, dout, lse, delta, lse2, num_bh, N, Npad);
+    else
+        return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
