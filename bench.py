@@ -342,15 +342,29 @@ def run_s2(args):
         ho, hl, hdq, hdk, hdv = (torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
                                  for t in (out, lse, dq, dk, dv))
         e2e_steps = max(1, min(args.steps, 5))
+        e2e_api = "s2_attn_fwd_bwd_host (C ABI, host buffers, H2D/kernels/D2H pipelined over 16 unit chunks)"
+        if world == 1:
+            # the host-resident data path of the public API: one call per step
+            hq4, hk4, hv4, hdo4 = (t.reshape(1, U, N_SEQ, D) for t in (hq, hk, hv, hdo))
+            ho4, hdq4 = ho.reshape(1, U, N_SEQ, D), hdq.reshape(1, U, N_SEQ, D)
+            hl4 = hl.reshape(1, U, N_SEQ)
+            hdk4, hdv4 = hdk.reshape(1, U, N_SEQ, D), hdv.reshape(1, U, N_SEQ, D)
+            ws_holder = [None]
 
-        def e2e_step():
-            q.copy_(hq, non_blocking=True)
-            k.copy_(hk, non_blocking=True)
-            v.copy_(hv, non_blocking=True)
-            do.copy_(hdo, non_blocking=True)
-            step()
-            for dst, src in ((ho, out), (hl, lse), (hdq, dq), (hdk, dk), (hdv, dv)):
-                dst.copy_(src, non_blocking=True)
+            def e2e_step():
+                ws_holder[0] = s2.s2_attn_fwd_bwd_host(plan, hq4, hk4, hv4, hdo4, ho4, hl4, hdq4, hdk4, hdv4,
+                                                       num_chunks=16, workspace=ws_holder[0])
+        else:
+            e2e_api = "torch copies from pinned host memory + s2_attn_fwd/bwd on this rank's units"
+
+            def e2e_step():
+                q.copy_(hq, non_blocking=True)
+                k.copy_(hk, non_blocking=True)
+                v.copy_(hv, non_blocking=True)
+                do.copy_(hdo, non_blocking=True)
+                step()
+                for dst, src in ((ho, out), (hl, lse), (hdq, dq), (hdk, dk), (hdv, dv)):
+                    dst.copy_(src, non_blocking=True)
 
         e2e_step()
         barrier()
@@ -366,7 +380,8 @@ def run_s2(args):
         h2d = sum(t.numel() * t.element_size() for t in (q, k, v, do))
         d2h = sum(t.numel() * t.element_size() for t in (out, lse, dq, dk, dv))
         line["e2e"] = {"value": 3.5 * tot_fwd_flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
-                       "ms_per_step": ems, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+                       "ms_per_step": ems, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "api": e2e_api}
 
     # ---- hybrid 24-layer mix of cfg3 (dense layers {0, 1}, configs/l1v15_dense01.json
     #      shape): one dense-causal layer through the same kernels (LayerStack),

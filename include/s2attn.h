@@ -200,6 +200,20 @@ int s2_attn_bwd_workspace_size(const s2_plan* plan, const s2_attn_bwd_args* args
 int s2_attn_bwd(s2_plan* plan, const s2_attn_bwd_args* args, void* workspace,
                 size_t workspace_bytes, s2_stream_t stream);
 
+/* ---- one layer's forward + backward on HOST buffers -------------------------
+ * The reference's data path (AttentionTensors in host memory, attention.hpp:
+ * 17-37) for bf16: every pointer in `args` (q, k, v, dout in; out, lse, dq, dk,
+ * dv out) is HOST memory, ideally pinned.  The (batch, kv-group) units are cut
+ * into num_chunks chunks whose H2D copy, forward + backward and D2H copy are
+ * pipelined on three streams (heads are independent, test_attention.cpp:
+ * 217-240), so the PCIe transfers overlap each other and the kernels.
+ * workspace: device memory of s2_attn_fwd_bwd_host_workspace_size bytes.
+ * Completion is ordered on `stream`. */
+int s2_attn_fwd_bwd_host_workspace_size(const s2_plan* plan, const s2_attn_bwd_args* args,
+                                        int num_chunks, size_t* bytes);
+int s2_attn_fwd_bwd_host(s2_plan* plan, const s2_attn_bwd_args* args, int num_chunks,
+                         void* workspace, size_t workspace_bytes, s2_stream_t stream);
+
 /* ---- decode over a per-(batch, kv-head) compacted KV cache --------------- */
 /* Cache contents follow simulate_decode_cache (analysis.cpp:57-104): key
  * block j is kept while the decode row bt <= evict_after[j]; for KV-efficient

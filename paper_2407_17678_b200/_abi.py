@@ -115,6 +115,9 @@ SIGNATURES = {
     "s2_attn_bwd_workspace_size": (_I, [_P, ctypes.POINTER(s2_attn_bwd_args),
                                         ctypes.POINTER(ctypes.c_size_t)]),
     "s2_attn_bwd": (_I, [_P, ctypes.POINTER(s2_attn_bwd_args), _P, ctypes.c_size_t, _P]),
+    "s2_attn_fwd_bwd_host_workspace_size": (_I, [_P, ctypes.POINTER(s2_attn_bwd_args), _I,
+                                                 ctypes.POINTER(ctypes.c_size_t)]),
+    "s2_attn_fwd_bwd_host": (_I, [_P, ctypes.POINTER(s2_attn_bwd_args), _I, _P, ctypes.c_size_t, _P]),
     "s2_kvcache_create": (_I, [_P, _I, _I, _I, ctypes.POINTER(_P)]),
     "s2_kvcache_destroy": (None, [_P]),
     "s2_kvcache_length": (_I, [_P, _IP]),

@@ -202,6 +202,39 @@ def s2_attn_bwd(plan: Plan, q, k, v, out, lse, dout, *, scale: Optional[float] =
     return dq, dk, dv
 
 
+def s2_attn_fwd_bwd_host(plan: Plan, q, k, v, dout, out, lse, dq, dk, dv, *,
+                         scale: Optional[float] = None, num_chunks: int = 4, stream=None,
+                         workspace=None):
+    """One layer's forward + backward on HOST tensors (pinned CPU torch tensors,
+    bf16; lse fp32): the reference API's host-resident data path.  The C ABI
+    pipelines H2D copies, kernels and D2H copies over `num_chunks` chunks of
+    (batch, kv-group) units (s2_attn_fwd_bwd_host).  Returns when the work is
+    queued on `stream`; synchronize before reading the outputs."""
+    import torch
+
+    for t in (q, k, v, dout, out, lse, dq, dk, dv):
+        if t.is_cuda:
+            raise _abi.S2InvalidArgument(1, "s2_attn_fwd_bwd_host takes host tensors")
+    a = _abi.s2_attn_bwd_args()
+    B, H, N, D = q.shape
+    f = a.fwd
+    f.dtype = _dtype_code(q)
+    f.batch, f.num_heads, f.num_kv_heads, f.seq_len, f.head_dim = B, H, k.shape[1], N, D
+    f.scale = 0.0 if scale is None else float(scale)
+    f.num_splits, f.num_units, f.unit_ids = 1, 0, None
+    f.q, f.k, f.v, f.out, f.lse = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr()
+    a.dout, a.dq, a.dk, a.dv = dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr()
+    ws = ctypes.c_size_t()
+    check(lib().s2_attn_fwd_bwd_host_workspace_size(plan.handle, ctypes.byref(a), num_chunks,
+                                                     ctypes.byref(ws)))
+    if workspace is None or workspace.numel() < ws.value:
+        workspace = torch.empty(ws.value, dtype=torch.uint8, device="cuda")
+    check(lib().s2_attn_fwd_bwd_host(plan.handle, ctypes.byref(a), num_chunks,
+                                     ctypes.c_void_p(workspace.data_ptr()), ws.value,
+                                     _stream_ptr(stream)))
+    return workspace
+
+
 def _autograd_fn():
     import torch
 

@@ -122,3 +122,26 @@ def test_hybrid_layer_stack_fwd_bwd():
         np.testing.assert_allclose(f(out), ro, **TOL)
         for g, r in ((dq, rq), (dk, rk), (dv, rv)):
             np.testing.assert_allclose(f(g), r, **TOL)
+
+
+def test_host_buffer_pipeline_matches_device_path():
+    """s2_attn_fwd_bwd_host (host tensors, chunked H2D / kernels / D2H on three
+    streams) returns exactly what the device path returns."""
+    import torch
+
+    cfg = single(2048, 64, 8, 4, 8, kv=4)
+    plan = s2.Plan.from_config(cfg)
+    B, H, Hkv, N, D = 2, 8, 4, 2048, 128
+    g = torch.Generator().manual_seed(9)
+    mk = lambda h: (torch.rand((B, h, N, D), generator=g) * 2 - 1).to(torch.bfloat16).pin_memory()  # noqa
+    q, k, v, do = mk(H), mk(Hkv), mk(Hkv), mk(H)
+    outs = [torch.empty_like(q).pin_memory(), torch.empty((B, H, N), dtype=torch.float32).pin_memory(),
+            torch.empty_like(q).pin_memory(), torch.empty_like(k).pin_memory(), torch.empty_like(v).pin_memory()]
+    for chunks in (1, 3, 8):
+        s2.s2_attn_fwd_bwd_host(plan, q, k, v, do, *outs, num_chunks=chunks)
+        torch.cuda.synchronize()
+        dev = [t.cuda() for t in (q, k, v, do)]
+        o, l = s2.s2_attn_fwd(plan, *dev[:3])
+        gq, gk, gv = s2.s2_attn_bwd(plan, *dev[:3], o, l, dev[3])
+        for a, b in zip(outs, (o, l, gq, gk, gv)):
+            assert torch.equal(a, b.cpu()), chunks
