@@ -203,10 +203,13 @@ __global__ void __launch_bounds__(384, 1)
                             const int row0 = en.qtile * 128 + half * 64;
                             *reinterpret_cast<uint4*>(gAux + st * C::kAux + kMeta) =
                                 make_uint4(static_cast<uint32_t>(row0), m0, m1, static_cast<uint32_t>(qbh));
-                            mbar_expect_tx(bar, 2 * C::kTile64 + 512);
+                            // debug 16 (timing experiments only, wrong results): skip the dO tile
+                            const bool half_bytes = (p.debug & 16) != 0;
+                            mbar_expect_tx(bar, (half_bytes ? 1 : 2) * C::kTile64 + 512);
                             for (int s = 0; s < C::kSub; ++s) {
                                 tma_load_3d(base + s * 8192, &tmQ, bar, s * 64, row0, qbh);
-                                tma_load_3d(base + C::kTile64 + s * 8192, &tmdO, bar, s * 64, row0, qbh);
+                                if (!half_bytes)
+                                    tma_load_3d(base + C::kTile64 + s * 8192, &tmdO, bar, s * 64, row0, qbh);
                             }
                             const size_t lo = static_cast<size_t>(qbh) * p.Npad + row0;
                             bulk_load(sAux + st * C::kAux, p.lse2 + lo, 256, bar);
@@ -763,7 +766,7 @@ cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CU
     const float sl2 = scale * 1.4426950408889634f;
     // debug bit 8 selects which kernel records the trace (0: dK/dV, 8: dQ)
     long long* tr = ((g_debug & 8) != 0) == (which == 1) ? g_trace : nullptr;
-    BwdParams pp{items, sched, entries, lse2, delta, nullptr, nullptr, N, Npad, hpg, sl2, scale, tr, g_debug & 7};
+    BwdParams pp{items, sched, entries, lse2, delta, nullptr, nullptr, N, Npad, hpg, sl2, scale, tr, g_debug & ~8};
     if (g_debug & 4) grid = 1;  // debug: isolate one CTA from memory-system contention
     if (D == 128)
         return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<128>, BwdCfg<128>::kDkvSmem, grid, q, dout, k, v, o0, o1, pp, stream)
