@@ -14,7 +14,7 @@ using namespace s2dev;
 // D[128 x N] = A[128 x K] * B[N x K]^T, both K-major bf16.
 __global__ void __launch_bounds__(128, 1)
     probe_ss_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
-                    int N, int K, float* D) {
+                    int N, int K, float* D, int a_in_tmem) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bars[2];
@@ -49,7 +49,14 @@ __global__ void __launch_bounds__(128, 1)
             const int sub = kk / 4, off = (kk % 4) * 32;
             const uint64_t ad = umma_desc_sw128(sA + sub * 16384 + off, 16, 1024);
             const uint64_t bd = umma_desc_sw128(sB + sub * N * 128 + off, 16, 1024);
-            mma_ss(tbase, ad, bd, idesc, kk > 0);
+            if (a_in_tmem) {
+                // A's K slice kk: smem (SW128 K-major) -> TMEM columns 256 + 8kk (128 lanes x 256 bit)
+                asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tbase + 256 + kk * 8), "l"(ad)
+                             : "memory");
+                mma_ts(tbase, tbase + 256 + kk * 8, bd, idesc, kk > 0);
+            } else {
+                mma_ss(tbase, ad, bd, idesc, kk > 0);
+            }
         }
         mma_commit(smem_u32(&bars[1]));
     }
@@ -134,13 +141,18 @@ static thread_local char g_msg[512];
 extern "C" const char* probe_last_error() { return g_msg; }
 
 // A: device bf16 [128][K]; B: device bf16 [N][K]; D: device f32 [128][N].
+extern "C" int probe_ss_tmem_a(const void* A, const void* B, int N, int K, float* D, int a_in_tmem);
 extern "C" int probe_ss(const void* A, const void* B, int N, int K, float* D) {
+    return probe_ss_tmem_a(A, B, N, K, D, 0);
+}
+// a_in_tmem: A staged smem -> TMEM with tcgen05.cp.128x256b, then TS MMAs
+extern "C" int probe_ss_tmem_a(const void* A, const void* B, int N, int K, float* D, int a_in_tmem) {
     try {
         const CUtensorMap mA = s2host::make_map_bf16_3d(A, K, 128, 1, 64, 128);
         const CUtensorMap mB = s2host::make_map_bf16_3d(B, K, N, 1, 64, N);
         const int smem = 1024 + (K / 64) * (16384 + N * 128);
         cudaFuncSetAttribute(probe_ss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        probe_ss_kernel<<<1, 128, smem>>>(mA, mB, N, K, D);
+        probe_ss_kernel<<<1, 128, smem>>>(mA, mB, N, K, D, a_in_tmem);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
             snprintf(g_msg, sizeof g_msg, "%s", cudaGetErrorString(e));

@@ -52,3 +52,23 @@ def test_probe_ts(KK, Dv):
     assert rc == 0, lib.probe_last_error()
     ref = P.to(torch.bfloat16).float() @ V.float()
     torch.testing.assert_close(O, ref, rtol=1e-3, atol=1e-3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,K", [(64, 128), (128, 128)])
+def test_probe_a_operand_copied_to_tmem(N, K):
+    """tcgen05.cp.128x256b of a SW128 K-major A tile (the MMA's own smem
+    descriptor) gives the TS-MMA A layout: same product as the SS MMA."""
+    import torch
+
+    lib = _lib()
+    torch.manual_seed(2)
+    A = torch.randn(128, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    D1 = torch.zeros(128, N, device="cuda")
+    D2 = torch.zeros(128, N, device="cuda")
+    assert lib.probe_ss_tmem_a(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()), N, K,
+                               ctypes.c_void_p(D1.data_ptr()), 0) == 0, lib.probe_last_error()
+    assert lib.probe_ss_tmem_a(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()), N, K,
+                               ctypes.c_void_p(D2.data_ptr()), 1) == 0, lib.probe_last_error()
+    assert torch.equal(D1, D2)
