@@ -505,7 +505,9 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
-    // TMEM: S[b] at 64b, dP[b] at 128+64b, dQ at 256.
+    // TMEM: Q at 0 and dO at 64 (the S / dP A operands, copied in with tcgen05.cp once
+    // per item: the per-step MMAs then read only the 2 KB K / V slices from shared
+    // memory), S[b] at 128+64b, dP[b] at 256+64b, dQ at 384.
 
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
@@ -555,6 +557,19 @@ __global__ void __launch_bounds__(384, 1)
                 const int qb = it_cnt % C::kQB;
                 const uint32_t qoff = (qb * 2 * C::kTile128) >> 4;
                 mbar_wait(smem_u32(&bar_qf[qb]), (it_cnt / C::kQB) & 1);
+                if (leader) {  // after the previous item's last S / dP MMAs (issue order)
+                    const uint64_t dq0 = dQ0 + qoff, ddo0 = ddO0 + qoff;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t ao = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                        tmem_cp_128x256b(tmem + kk * 8, dq0 + ao);
+                        tmem_cp_128x256b(tmem + 64 + kk * 8, ddo0 + ao);
+                    }
+                    // Q / dO now live in TMEM: the smem buffer may be refilled once the
+                    // copies are done (and the epilogue staged in it has been stored)
+                    mma_commit(smem_u32(&bar_qe[qb]));
+                }
+                __syncwarp();
                 bool first = true;
                 auto accumulate = [&](uint32_t n, int st) {
                     const int b = n & 1;
@@ -567,7 +582,7 @@ __global__ void __launch_bounds__(384, 1)
                     if (leader) {
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)  // dQ += dS K  (K chunk as MN-major B)
-                            mma_ts(tmem + 256, tmem + 128 + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
+                            mma_ts(tmem + 384, tmem + 256 + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
                                    dst + ((kk * 2048) >> 4), idA, (first && kk == 0) ? 0u : 1u);
                         mma_commit(smem_u32(&bar_se[st]));
                     }
@@ -586,15 +601,13 @@ __global__ void __launch_bounds__(384, 1)
                     if (leader) {
 #pragma unroll
                         for (int kk = 0; kk < D / 16; ++kk) {
-                            const uint32_t ao = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
                             const uint32_t bo = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
-                            mma_ss(tmem + b * 64, dQ0 + qoff + ao, dst + bo, idS, kk > 0);
-                            mma_ss(tmem + 128 + b * 64, ddO0 + qoff + ao, dst + ((C::kTile64 >> 4) + bo), idS,
+                            // S = Q K^T, dP = dO V^T with Q / dO from TMEM (TS)
+                            mma_ts(tmem + 128 + b * 64, tmem + kk * 8, dst + bo, idS, kk > 0);
+                            mma_ts(tmem + 256 + b * 64, tmem + 64 + kk * 8, dst + ((C::kTile64 >> 4) + bo), idS,
                                    kk > 0);
                         }
                         mma_commit(smem_u32(&bar_s[b]));
-                        // Q / dO feed only S / dP: release them after the item's last ones
-                        if (n == chunk_cnt - 1) mma_commit(smem_u32(&bar_qe[qb]));
                     }
                     __syncwarp();
                     S2TRACE(2, n_glob);
@@ -604,7 +617,6 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 if (prev_st >= 0) accumulate(prev_n, prev_st);
                 if (leader) {
-                    if (chunk_cnt == 0) mma_commit(smem_u32(&bar_qe[qb]));  // (user CSR with empty rows)
                     mma_commit(smem_u32(&bar_af));
                 }
                 __syncwarp();
@@ -633,8 +645,8 @@ __global__ void __launch_bounds__(384, 1)
                 if (tid == 128) S2TRACE(6, n_glob);
                 tc_fence_after();
                 uint32_t su[32], du[32];
-                tmem_ld32(tmem + b * 64 + wg * 32 + lane_off, su);
-                tmem_ld32(tmem + 128 + b * 64 + wg * 32 + lane_off, du);
+                tmem_ld32(tmem + 128 + b * 64 + wg * 32 + lane_off, su);
+                tmem_ld32(tmem + 256 + b * 64 + wg * 32 + lane_off, du);
                 const uint32_t bits = (static_cast<uint32_t>(ch.y) >> (rg * 4)) & 0xFu;
                 const bool on0 = (bits >> (wg * 2)) & 1u, on1 = (bits >> (wg * 2 + 1)) & 1u;
                 const int k0 = ch.x * 64 + wg * 32;
@@ -662,7 +674,7 @@ __global__ void __launch_bounds__(384, 1)
                         dk[c >> 1] = pack_bf16(dv[0], dv[1]);
                     }
                 }
-                tmem_st16(tmem + 128 + b * 64 + wg * 32 + lane_off, dk);  // own columns only
+                tmem_st16(tmem + 256 + b * 64 + wg * 32 + lane_off, dk);  // own columns only
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(smem_u32(&bar_p[b]));
@@ -680,7 +692,7 @@ __global__ void __launch_bounds__(384, 1)
             uint32_t acc[D / 2];
 #pragma unroll
             for (int c = 0; c < D / 64; ++c)
-                tmem_ld32(tmem + 256 + wg * (D / 2) + c * 32 + lane_off,
+                tmem_ld32(tmem + 384 + wg * (D / 2) + c * 32 + lane_off,
                           *reinterpret_cast<uint32_t(*)[32]>(acc + 32 * c));
             tmem_ld_wait();
             tc_fence_before();

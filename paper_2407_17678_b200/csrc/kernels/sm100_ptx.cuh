@@ -151,6 +151,12 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// TMEM[128 lanes x 8 columns] <- one SW128 K-major smem slice of 128 rows x 16 bf16
+// (the slice's MMA descriptor): the TS-MMA A-operand layout.  Ordered with
+// tcgen05.mma in the issuing thread's pipeline.
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 // Arrive on an mbarrier once every previously issued tcgen05.mma of this
 // thread has completed (implies tcgen05.fence::before_thread_sync).
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
