@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(384, 1)
     // bar_kve[kb]: K/V buffer kb is free (its item's last S^T/dP^T MMAs done AND both
     // epilogue TMA stores, staged in it, have read it): count 3
     __shared__ uint64_t bar_kvf[2], bar_kve[2], bar_sf[NST], bar_se[NST], bar_s[2], bar_p[2], bar_af, bar_ae;
+    __shared__ uint64_t bar_dpf;  // the elementwise warps have read dP^T (its single TMEM buffer is free)
     __shared__ uint32_t tmem_base_s;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // K/V buffer kb: K at sK + kb * 2 * kTile128, V right after it
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(smem_u32(&bar_s[i]), 1);
             mbar_init(smem_u32(&bar_p[i]), 256);
         }
+        mbar_init(smem_u32(&bar_dpf), 256);
         fence_mbar_init();
     }
     if (warp == 2) {
@@ -167,7 +169,12 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
-    // TMEM: S^T[b] at 64b, dP^T[b] at 128+64b, dV at 256, dK at 384.
+    // TMEM: V at 0 (the dP^T A operand: copied in once per item with tcgen05.cp, so
+    // the per-step dP^T MMAs read only the 2 KB dO slices from shared memory),
+    // S^T[b] at 64+64b (the elementwise warps write P^T and dS^T back into it: warp
+    // group w's 32 columns hold P^T at +0..15 and dS^T at +16..31), dP^T at 192
+    // (single buffer: read into registers at the start of each elementwise pass),
+    // dV at 256, dK at 384.
     const int i_beg = p.sched[blockIdx.x], i_end = p.sched[blockIdx.x + 1];
 
     if (warp < 4) {
@@ -245,6 +252,12 @@ __global__ void __launch_bounds__(384, 1)
                 const int kb = it_cnt & 1;
                 const uint32_t kvoff = (kb * 2 * C::kTile128) >> 4;
                 mbar_wait(smem_u32(&bar_kvf[kb]), (it_cnt >> 1) & 1);
+                if (leader) {  // V -> TMEM, after the previous item's last dP^T (issue order)
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        tmem_cp_128x256b(tmem + kk * 8, dV0 + kvoff + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4));
+                }
+                __syncwarp();
                 auto accumulate = [&](uint32_t n, int st, bool first) {
                     const int b = n & 1;
                     S2TRACE(3, n);
@@ -262,10 +275,11 @@ __global__ void __launch_bounds__(384, 1)
                         for (int kk = 0; kk < ((p.debug & 2) ? 0 : 4); ++kk) {
                             const uint32_t acc = (first && kk == 0) ? 0u : 1u;
                             // K slice kk of P^T / dS^T: WG (kk >> 1) stored it at 32*(kk>>1) + 8*(kk&1)
-                            const uint32_t ac = b * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+                            // (+16 for dS^T) of the step's S^T buffer
+                            const uint32_t ac = 64 + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
                             // dV += P^T dO ; dK += dS^T Q   (B operands MN-major)
                             mma_ts(tmem + 256, tmem + ac, dst + ((C::kTile64 + kk * 2048) >> 4), idA, acc);
-                            mma_ts(tmem + 384, tmem + 128 + ac, dst + ((kk * 2048) >> 4), idA, acc);
+                            mma_ts(tmem + 384, tmem + ac + 16, dst + ((kk * 2048) >> 4), idA, acc);
                         }
                         mma_commit(smem_u32(&bar_se[st]));
                     }
@@ -281,13 +295,20 @@ __global__ void __launch_bounds__(384, 1)
                     const int b = n & 1;
                     if (leader) {
 #pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk) {
+                        for (int kk = 0; kk < D / 16; ++kk) {  // S^T = K Q^T  (K-major x K-major)
                             const uint32_t ao = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
                             const uint32_t bo = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
-                            // S^T = K Q^T ; dP^T = V dO^T  (K-major x K-major)
-                            mma_ss(tmem + b * 64, dK0 + kvoff + ao, dst + bo, idS, kk > 0);
-                            mma_ss(tmem + 128 + b * 64, dV0 + kvoff + ao, dst + ((C::kTile64 >> 4) + bo), idS,
-                                   kk > 0);
+                            mma_ss(tmem + 64 + b * 64, dK0 + kvoff + ao, dst + bo, idS, kk > 0);
+                        }
+                    }
+                    __syncwarp();
+                    // dP^T(n) overwrites dP^T(n-1): the elementwise pass n-1 must have read it
+                    if (n > 0) mbar_wait(smem_u32(&bar_dpf), (n - 1) & 1);
+                    if (leader) {
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {  // dP^T = V dO^T  (V from TMEM)
+                            const uint32_t bo = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
+                            mma_ts(tmem + 192, tmem + kk * 8, dst + ((C::kTile64 >> 4) + bo), idS, kk > 0);
                         }
                         mma_commit(smem_u32(&bar_s[b]));
                         // K / V are read by the S^T / dP^T MMAs only: release them after
@@ -330,12 +351,13 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_after();
                 if (p.debug & 1) {
                     tc_fence_before();
+                    mbar_arrive(smem_u32(&bar_dpf));
                     mbar_arrive(smem_u32(&bar_p[b]));
                     continue;
                 }
                 uint32_t su[32], du[32];
-                tmem_ld32(tmem + b * 64 + wg * 32 + lane_off, su);
-                tmem_ld32(tmem + 128 + b * 64 + wg * 32 + lane_off, du);
+                tmem_ld32(tmem + 64 + b * 64 + wg * 32 + lane_off, su);
+                tmem_ld32(tmem + 192 + wg * 32 + lane_off, du);
                 // lse2 / delta / meta of this stage: shared-space vector loads
                 // (broadcast).  They were written by a bulk copy / the producer:
                 // observe the stage barrier ourselves (already complete; the
@@ -355,6 +377,8 @@ __global__ void __launch_bounds__(384, 1)
                     dlv[c] = d4.x; dlv[c + 1] = d4.y; dlv[c + 2] = d4.z; dlv[c + 3] = d4.w;
                 }
                 tmem_ld_wait();
+                tc_fence_before();
+                mbar_arrive(smem_u32(&bar_dpf));  // dP^T is in registers: the next dP^T may land
                 uint32_t pk[16], dk[16];
                 if (on0 && on1 && key_pos <= q0) {
                     // fully attended 32 columns, no causal cut: no per-element masking
@@ -382,10 +406,10 @@ __global__ void __launch_bounds__(384, 1)
                         dk[c >> 1] = pack_bf16(dv[0], dv[1]);
                     }
                 }
-                // P^T / dS^T of my 32 q columns go into the first half of the
-                // columns I read (never into the other WG's unread columns)
-                tmem_st16(tmem + b * 64 + wg * 32 + lane_off, pk);
-                tmem_st16(tmem + 128 + b * 64 + wg * 32 + lane_off, dk);
+                // P^T / dS^T of my 32 q columns go into the 32 S^T columns I read
+                // (never into the other WG's unread columns)
+                tmem_st16(tmem + 64 + b * 64 + wg * 32 + lane_off, pk);
+                tmem_st16(tmem + 64 + b * 64 + wg * 32 + 16 + lane_off, dk);
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(smem_u32(&bar_p[b]));
