@@ -345,23 +345,10 @@ __global__ void __launch_bounds__(384, 1)
             for (int s = 0; s < it.nsteps; ++s, ++st_it) {
                 const int st = st_it % NST;
                 const int b = st_it & 1;
-                if (tid == 128) S2TRACE(5, st_it);
-                mbar_wait(smem_u32(&bar_s[b]), (st_it >> 1) & 1);
-                if (tid == 128) S2TRACE(6, st_it);
-                tc_fence_after();
-                if (p.debug & 1) {
-                    tc_fence_before();
-                    mbar_arrive(smem_u32(&bar_dpf));
-                    mbar_arrive(smem_u32(&bar_p[b]));
-                    continue;
-                }
-                uint32_t su[32], du[32];
-                tmem_ld32(tmem + 64 + b * 64 + wg * 32 + lane_off, su);
-                tmem_ld32(tmem + 192 + wg * 32 + lane_off, du);
-                // lse2 / delta / meta of this stage: shared-space vector loads
-                // (broadcast).  They were written by a bulk copy / the producer:
-                // observe the stage barrier ourselves (already complete; the
-                // stage cannot be refilled before our P arrives).
+                // lse2 / delta / meta of this stage first (shared-space vector loads,
+                // broadcast), while S^T / dP^T are still being computed.  They were
+                // written by a bulk copy / the producer: observe the stage barrier
+                // ourselves (the stage cannot be refilled before our P arrives).
                 mbar_wait(smem_u32(&bar_sf[st]), (st_it / NST) & 1);
                 const uint4 meta = *reinterpret_cast<const uint4*>(gAux + st * C::kAux + kMeta);
                 const uint32_t m = key_ok ? (hk ? meta.z : meta.y) : 0u;
@@ -376,6 +363,19 @@ __global__ void __launch_bounds__(384, 1)
                     l2v[c] = a.x; l2v[c + 1] = a.y; l2v[c + 2] = a.z; l2v[c + 3] = a.w;
                     dlv[c] = d4.x; dlv[c + 1] = d4.y; dlv[c + 2] = d4.z; dlv[c + 3] = d4.w;
                 }
+                if (tid == 128) S2TRACE(5, st_it);
+                mbar_wait(smem_u32(&bar_s[b]), (st_it >> 1) & 1);
+                if (tid == 128) S2TRACE(6, st_it);
+                tc_fence_after();
+                if (p.debug & 1) {
+                    tc_fence_before();
+                    mbar_arrive(smem_u32(&bar_dpf));
+                    mbar_arrive(smem_u32(&bar_p[b]));
+                    continue;
+                }
+                uint32_t su[32], du[32];
+                tmem_ld32(tmem + 64 + b * 64 + wg * 32 + lane_off, su);
+                tmem_ld32(tmem + 192 + wg * 32 + lane_off, du);
                 tmem_ld_wait();
                 tc_fence_before();
                 mbar_arrive(smem_u32(&bar_dpf));  // dP^T is in registers: the next dP^T may land
