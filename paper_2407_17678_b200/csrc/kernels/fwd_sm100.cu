@@ -1,7 +1,6 @@
 // S2-Attention forward, sm_100a.  Persistent CTAs; each work item is a PAIR
 // of adjacent 128-row query tiles of one (batch, head) that share every K/V
-// load (the union of their chunk lists), FA4-style ping-pong between two
-// softmax warpgroups so one tile's softmax overlaps the other tile's MMAs.
+// load (the union of their chunk lists), with one softmax warpgroup per tile.
 //
 // Replaces the reference's streaming kernel process_query_block
 // (/root/reference/proj/src/attention.cpp:26-98) and its OpenMP driver
@@ -11,16 +10,21 @@
 // fixed per item and nothing is reduced across CTAs: deterministic, and
 // independent of head position (test_attention.cpp:217-257).
 //
+// Chunk-granular pipeline: every step is one 64-key chunk.  Each tile's 128
+// S columns hold TWO chunk scores (S(k) in half k&1), so the MMA warp issues
+// S_t(k+1) before O_t += P_t(k) V(k): the next scores are computed while the
+// softmax of this chunk runs, instead of after it.
+//
 // Warp roles (384 threads, 1 CTA / SM; setmaxnreg moves registers from the
 // control warpgroup (56/thread) to the two softmax warpgroups (224/thread)):
-//   warp 0      TMA producer: Q tiles, K/V chunk pairs into an NST ring
-//   warp 1      MMA issuer:  per step n, per tile t: O_t += P_t(n-1) V(n-1)  (TS)
-//                                                   S_t  = Q_t K(n)^T     (SS)
+//   warp 0      TMA producer: Q tiles, one K/V chunk per NST ring stage
+//   warp 1      MMA issuer:  per chunk j: S_t(j) = Q_t K(j)^T for both tiles (SS,
+//               N=64), then O_t += P_t(j-1) V(j-1) (TS, K=64)
 //   warp 2      TMEM allocator
 //   warps 4-7   softmax of tile 0 (thread = query row = TMEM lane), epilogue
 //   warps 8-11  softmax of tile 1
-// TMEM (512 columns): tile t owns [256t, 256t+256): S at +0 (P aliases its
-// first 64 columns as packed bf16x2), O at +128.
+// TMEM (512 columns): tile t owns [256t, 256t+256): S halves at +0 / +64 (P
+// of a chunk overwrites the first 32 columns of its half as bf16x2), O at +128.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -61,10 +65,10 @@ struct Fwd2Params {
 template <int D>
 struct Fwd2Cfg {
     static constexpr int kSub = D / 64;
-    static constexpr int kQBytes = kSub * 16384;   // 128 rows
-    static constexpr int kKBytes = kSub * 16384;   // 128 keys
-    static constexpr int kNST = D == 128 ? 2 : 4;
-    static constexpr int kStageBytes = 2 * kKBytes;
+    static constexpr int kQBytes = kSub * 16384;  // 128 rows
+    static constexpr int kCBytes = kSub * 8192;   // one 64-key chunk of K (or V)
+    static constexpr int kNST = D == 128 ? 4 : 8;
+    static constexpr int kStageBytes = 2 * kCBytes;
     static constexpr int kSmem = 1024 + 2 * kQBytes + kNST * kStageBytes;
 };
 
@@ -94,8 +98,12 @@ __global__ void __launch_bounds__(384, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_qf[2], bar_qe[2], bar_kf[NST], bar_vf[NST], bar_ke[NST];
-    __shared__ uint64_t bar_sf[2], bar_pf[2], bar_of[2], bar_oe[2];
+    __shared__ uint64_t bar_qf[2], bar_qe[2], bar_kf[NST], bar_ke[NST];
+    // bar_pv[t]: completes once per P V of tile t (the softmax waits on it only to
+    // rescale O, which the previous chunk's P V may still be accumulating into).
+    // S / P barriers are per (tile, S half): the MMA warp runs one chunk ahead of
+    // the softmax, so a single barrier could complete two phases ahead of a waiter.
+    __shared__ uint64_t bar_sf[2][2], bar_pf[2][2], bar_of[2], bar_oe[2], bar_pv[2];
     __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x;
@@ -107,14 +115,16 @@ __global__ void __launch_bounds__(384, 1)
         for (int i = 0; i < 2; ++i) {
             mbar_init(smem_u32(&bar_qf[i]), 1);
             mbar_init(smem_u32(&bar_qe[i]), 1);
-            mbar_init(smem_u32(&bar_sf[i]), 1);
-            mbar_init(smem_u32(&bar_pf[i]), 128);
+            for (int j = 0; j < 2; ++j) {
+                mbar_init(smem_u32(&bar_sf[i][j]), 1);
+                mbar_init(smem_u32(&bar_pf[i][j]), 128);
+            }
             mbar_init(smem_u32(&bar_of[i]), 1);
             mbar_init(smem_u32(&bar_oe[i]), 128);
+            mbar_init(smem_u32(&bar_pv[i]), 1);
         }
         for (int i = 0; i < NST; ++i) {
             mbar_init(smem_u32(&bar_kf[i]), 1);
-            mbar_init(smem_u32(&bar_vf[i]), 1);
             mbar_init(smem_u32(&bar_ke[i]), 1);
         }
         fence_mbar_init();
@@ -151,126 +161,131 @@ __global__ void __launch_bounds__(384, 1)
                     ++q_use[t];
                 }
                 const PairStep* steps = p.steps + it.step_off;
-                for (int n = 0; n < it.nsteps; ++n, ++kv_it) {
-                    const int st = kv_it % NST;
-                    if (kv_it >= NST) mbar_wait(smem_u32(&bar_ke[st]), ((kv_it / NST) + 1) & 1);
-                    const PairStep s = steps[n];
-                    const int nc = s.c1 >= 0 ? 2 : 1;
-                    const uint32_t sK = sKV + st * C::kStageBytes;
-                    const uint32_t sV = sK + C::kKBytes;
-                    mbar_expect_tx(smem_u32(&bar_kf[st]), nc * C::kSub * 8192);
-                    for (int h = 0; h < nc; ++h)
-                        for (int sb = 0; sb < C::kSub; ++sb)
-                            tma_load_3d_hint(sK + sb * 16384 + h * 8192, &tmK, smem_u32(&bar_kf[st]),
-                                             sb * 64, (h ? s.c1 : s.c0) * 64, kvbh, keep);
-                    mbar_expect_tx(smem_u32(&bar_vf[st]), nc * C::kSub * 8192);
-                    for (int h = 0; h < nc; ++h)
-                        for (int sb = 0; sb < C::kSub; ++sb)
-                            tma_load_3d_hint(sV + sb * 16384 + h * 8192, &tmV, smem_u32(&bar_vf[st]),
-                                             sb * 64, (h ? s.c1 : s.c0) * 64, kvbh, keep);
+                for (int n = 0; n < it.nsteps; ++n) {
+                    const PairStep ps = steps[n];
+                    for (int h = 0; h < 2; ++h) {
+                        const int chunk = h ? ps.c1 : ps.c0;
+                        if (chunk < 0) continue;
+                        const int st = kv_it % NST;
+                        if (kv_it >= NST) mbar_wait(smem_u32(&bar_ke[st]), ((kv_it / NST) + 1) & 1);
+                        const uint32_t sK = sKV + st * C::kStageBytes, sV = sK + C::kCBytes;
+                        const uint32_t bar = smem_u32(&bar_kf[st]);
+                        mbar_expect_tx(bar, 2 * C::kCBytes);
+                        for (int sb = 0; sb < C::kSub; ++sb) {
+                            tma_load_3d_hint(sK + sb * 8192, &tmK, bar, sb * 64, chunk * 64, kvbh, keep);
+                            tma_load_3d_hint(sV + sb * 8192, &tmV, bar, sb * 64, chunk * 64, kvbh, keep);
+                        }
+                        ++kv_it;
+                    }
                 }
             }
         } else if (warp == 1) {
             // ------------------------------------------------------ MMA issuer
             // Whole warp on warp-uniform values, one elected lane issues (the
             // descriptors stay in uniform registers: no per-MMA waterfall).
-            constexpr uint32_t idS128 = umma_idesc_bf16(128, 128, 0, 0);
-            constexpr uint32_t idS64 = umma_idesc_bf16(128, 64, 0, 0);
+            constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);
             constexpr uint32_t idO = umma_idesc_bf16(128, D, 0, 1);
             const bool leader = elect_one();
             const uint64_t dQ0 = umma_desc_sw128(sQ0, 16, 1024);
             const uint64_t dKV0 = umma_desc_sw128(sKV, 16, 1024);
-            const uint64_t dVmn0 = umma_desc_sw128(sKV + C::kKBytes, 16384, 1024);
+            const uint64_t dVmn0 = umma_desc_sw128(sKV + C::kCBytes, 8192, 1024);
             uint32_t kv_it = 0, q_use[2] = {0, 0}, p_cnt[2] = {0, 0}, o_use[2] = {0, 0};
+            uint32_t k_cnt[2] = {0, 0};  // S of tile t issued so far (global): its S half
             const int i_end = p.sched[blockIdx.x + 1];
             for (int i = p.sched[blockIdx.x]; i < i_end; ++i) {
                 const int nsteps = warp_uniform(p.items[i].nsteps);
                 const bool has_b = warp_uniform(p.items[i].has_b) != 0;
-                const int64_t step_off = p.items[i].step_off;
-                const PairStep* steps = p.steps + step_off;
+                const PairStep* steps = p.steps + p.items[i].step_off;
                 const bool has[2] = {true, has_b};
                 for (int t = 0; t < 2; ++t)
                     if (has[t]) mbar_wait(smem_u32(&bar_qf[t]), q_use[t] & 1);
-                int pend[2] = {-1, -1};     // step whose P awaits its PV
-                int pend_half[2] = {0, 0};  // 0: both halves, 1: half 0 only, 2: half 1 only
+                int pend_st[2] = {-1, -1};   // stage of the chunk whose P V is pending
+                uint32_t pend_half[2] = {0, 0};
                 bool first_pv[2] = {true, true};
-                PairStep nxt = steps[0];  // software-pipelined step descriptor
-                for (int n = 0; n <= nsteps; ++n) {
-                    uint32_t mA0 = 0, mA1 = 0, mB0 = 0, mB1 = 0;
-                    uint32_t st = 0;
-                    bool k_ready = false;
-                    if (n < nsteps) {
-                        const PairStep sp = nxt;
-                        if (n + 1 < nsteps) nxt = steps[n + 1];
-                        mA0 = warp_uniform(sp.a0);
-                        mA1 = warp_uniform(sp.a1);
-                        mB0 = warp_uniform(sp.b0);
-                        mB1 = warp_uniform(sp.b1);
-                        st = (kv_it + n) % NST;
+                int prev_st = -1;             // stage of the previous chunk (released after its P Vs)
+                auto issue_pv = [&](int t) {
+                    const uint32_t tS = tmem + t * 256, tO = tS + 128;
+                    mbar_wait(smem_u32(&bar_pf[t][p_cnt[t] & 1]), (p_cnt[t] >> 1) & 1);
+                    ++p_cnt[t];
+                    if (first_pv[t] && o_use[t] > 0) mbar_wait(smem_u32(&bar_oe[t]), (o_use[t] - 1) & 1);
+                    tc_fence_after();  // P was written to TMEM by tcgen05.st
+                    const uint64_t dv = dVmn0 + static_cast<uint64_t>((pend_st[t] * C::kStageBytes) >> 4);
+                    if (leader) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma_ts(tO, tS + pend_half[t] * 64 + kk * 8, dv + ((kk * 2048) >> 4), idO,
+                                   (first_pv[t] && kk == 0) ? 0u : 1u);
+                        mma_commit(smem_u32(&bar_pv[t]));
                     }
+                    __syncwarp();
+                    first_pv[t] = false;
+                    pend_st[t] = -1;
+                };
+                PairStep nxt = steps[0];
+                for (int n = 0; n < nsteps; ++n) {
+                    const PairStep ps = nxt;
+                    if (n + 1 < nsteps) nxt = steps[n + 1];
+                    for (int h = 0; h < 2; ++h) {
+                        const int chunk = warp_uniform(h ? ps.c1 : ps.c0);
+                        if (chunk < 0) continue;
+                        const uint32_t mk[2] = {warp_uniform(h ? ps.a1 : ps.a0), warp_uniform(h ? ps.b1 : ps.b0)};
+                        const int st = kv_it % NST;
+                        mbar_wait(smem_u32(&bar_kf[st]), (kv_it / NST) & 1);
+                        const uint64_t dk = dKV0 + static_cast<uint64_t>((st * C::kStageBytes) >> 4);
+                        // S_t(j) for both tiles first: they run while P_t(j-1) is computed
+                        uint32_t s_half[2] = {0, 0};
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
-                        const uint32_t tS = tmem + t * 256, tO = tS + 128;
-                        if (pend[t] >= 0) {
-                            const uint32_t sm = (kv_it + pend[t]) % NST;
-                            mbar_wait(smem_u32(&bar_vf[sm]), ((kv_it + pend[t]) / NST) & 1);
-                            if (t == 0 && lane == 0) S2FTRACE(0, p_cnt[0]);
-                            mbar_wait(smem_u32(&bar_pf[t]), p_cnt[t] & 1);
-                            if (t == 0 && lane == 0) S2FTRACE(1, p_cnt[0]);
-                            ++p_cnt[t];
-                            if (first_pv[t] && o_use[t] > 0)
-                                mbar_wait(smem_u32(&bar_oe[t]), (o_use[t] - 1) & 1);
-                            tc_fence_after();  // P was written to TMEM by tcgen05.st
-                            const uint64_t dv = dVmn0 + static_cast<uint64_t>(
-                                (sm * C::kStageBytes + (pend_half[t] == 2 ? 8192u : 0u)) >> 4);
+                        for (int t = 0; t < 2; ++t) {
+                            if (!has[t] || !mk[t]) continue;
+                            s_half[t] = k_cnt[t] & 1;
+                            ++k_cnt[t];
+                            const uint32_t tS = tmem + t * 256 + s_half[t] * 64;
+                            const uint64_t dq = dQ0 + static_cast<uint64_t>((t * C::kQBytes) >> 4);
                             if (leader) {
-                                if (pend_half[t] == 0) {
 #pragma unroll
-                                    for (int kk = 0; kk < 8; ++kk)
-                                        mma_ts(tO, tS + kk * 8, dv + ((kk * 2048) >> 4), idO,
-                                               (first_pv[t] && kk == 0) ? 0u : 1u);
-                                } else {
-#pragma unroll
-                                    for (int kk = 0; kk < 4; ++kk)
-                                        mma_ts(tO, tS + kk * 8, dv + ((kk * 2048) >> 4), idO,
-                                               (first_pv[t] && kk == 0) ? 0u : 1u);
+                                for (int kk = 0; kk < D / 16; ++kk) {
+                                    const uint32_t oq = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                                    const uint32_t ok = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
+                                    mma_ss(tS, dq + oq, dk + ok, idS, kk > 0);
                                 }
+                                mma_commit(smem_u32(&bar_sf[t][s_half[t]]));
                             }
                             __syncwarp();
-                            first_pv[t] = false;
-                            pend[t] = -1;
                         }
-                        if (n < nsteps && has[t]) {
-                            const uint32_t m0 = t ? mB0 : mA0, m1 = t ? mB1 : mA1;
-                            if (m0 | m1) {
-                                if (!k_ready) {
-                                    if (lane == 0) S2FTRACE(2, kv_it + n);
-                                    mbar_wait(smem_u32(&bar_kf[st]), ((kv_it + n) / NST) & 1);
-                                    if (lane == 0) S2FTRACE(3, kv_it + n);
-                                    k_ready = true;
-                                }
-                                const int half = (m0 && m1) ? 0 : (m0 ? 1 : 2);
-                                const uint64_t dq = dQ0 + static_cast<uint64_t>((t * C::kQBytes) >> 4);
-                                const uint64_t dk = dKV0 + static_cast<uint64_t>(
-                                    (st * C::kStageBytes + (half == 2 ? 8192u : 0u)) >> 4);
-                                if (leader) {
+                        // then the pending P V of each tile (chunk j-1 or earlier)
 #pragma unroll
-                                    for (int kk = 0; kk < D / 16; ++kk) {
-                                        const uint32_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-                                        mma_ss(tS, dq + o, dk + o, half == 0 ? idS128 : idS64, kk > 0);
-                                    }
-                                    mma_commit(smem_u32(&bar_sf[t]));
-                                }
-                                __syncwarp();
-                                pend[t] = n;
-                                pend_half[t] = half;
-                            }
+                        for (int t = 0; t < 2; ++t)
+                            if (pend_st[t] >= 0 && (has[t] && mk[t])) issue_pv(t);
+                        // chunk j-1's stage is free once every P V reading it is issued
+                        if (prev_st >= 0 && pend_st[0] != prev_st && pend_st[1] != prev_st) {
+                            if (leader) mma_commit(smem_u32(&bar_ke[prev_st]));
+                            __syncwarp();
+                            prev_st = -1;
                         }
+#pragma unroll
+                        for (int t = 0; t < 2; ++t)
+                            if (has[t] && mk[t]) {
+                                pend_st[t] = st;
+                                pend_half[t] = s_half[t];
+                            }
+                        if (prev_st >= 0) {  // a tile skipped chunk j: its older P V holds prev_st
+                            // (flush: issue the held P V now so the stage can be released)
+#pragma unroll
+                            for (int t = 0; t < 2; ++t)
+                                if (pend_st[t] == prev_st) issue_pv(t);
+                            if (leader) mma_commit(smem_u32(&bar_ke[prev_st]));
+                            __syncwarp();
+                        }
+                        prev_st = st;
+                        ++kv_it;
                     }
-                    if (n >= 1) {
-                        if (leader) mma_commit(smem_u32(&bar_ke[(kv_it + n - 1) % NST]));
-                        __syncwarp();
-                    }
+                }
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+                    if (pend_st[t] >= 0) issue_pv(t);
+                if (prev_st >= 0) {
+                    if (leader) mma_commit(smem_u32(&bar_ke[prev_st]));
+                    __syncwarp();
                 }
                 if (leader)
                     for (int t = 0; t < 2; ++t)
@@ -284,7 +299,6 @@ __global__ void __launch_bounds__(384, 1)
                         ++o_use[t];
                         ++q_use[t];
                     }
-                kv_it += nsteps;
             }
         }
     } else {
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t tS = tmem + t * 256 + lane_off, tO = tS + 128;
         const int rg = r >> 4;
         const float sl2 = p.scale_log2;
-        uint32_t s_cnt = 0, o_cnt = 0;
+        uint32_t s_cnt = 0, o_cnt = 0, k_cnt = 0;
         for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i) {
             const PairItem it = p.items[i];
             if (t == 1 && !it.has_b) continue;
@@ -308,87 +322,75 @@ __global__ void __launch_bounds__(384, 1)
             for (int n = 0; n < it.nsteps; ++n) {
                 const PairStep s = nxt;
                 if (n + 1 < it.nsteps) nxt = steps[n + 1];
-                const uint32_t m0 = t ? s.b0 : s.a0, m1 = t ? s.b1 : s.a1;
-                if (!(m0 | m1)) continue;
-                const bool both = m0 && m1;
-                if (r == 0) S2FTRACE(4 + 2 * t, s_cnt);
-                mbar_wait(smem_u32(&bar_sf[t]), s_cnt & 1);
-                if (r == 0) S2FTRACE(5 + 2 * t, s_cnt);
-                ++s_cnt;
-                tc_fence_after();
-                float sv[128];
-                {
-                    // all column chunks in flight, one wait
-                    uint32_t* u = reinterpret_cast<uint32_t*>(sv);
-                    tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(u));
-                    tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
-                    if (both) {
-                        tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(u + 64));
-                        tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(u + 96));
-                    }
-                    tmem_ld_wait();
-                    if (!both) {
-#pragma unroll
-                        for (int j = 64; j < 128; ++j) sv[j] = -INFINITY;
-                    }
-                }
-                if (both) {
-                    apply_mask(sv, s.c0, m0, rg, q_pos, row0);
-                    apply_mask(sv + 64, s.c1, m1, rg, q_pos, row0);
-                } else {
-                    apply_mask(sv, m0 ? s.c0 : s.c1, m0 ? m0 : m1, rg, q_pos, row0);
-                }
-                // row max: 8 independent chains (a single chain is ~64 dependent FMNMX3)
-                float mxa[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) mxa[k] = fmaxf(sv[k], sv[k + 8]);
-#pragma unroll
-                for (int j = 16; j < 128; j += 16)
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) mxa[k] = fmaxf(mxa[k], fmaxf(sv[j + k], sv[j + k + 8]));
-                const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                                       fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-                const float m_tile = mx * sl2;
-                float m_use = m_run;
-                bool rescale = false;
-                if (m_tile > m_run) {
-                    if (m_run == -INFINITY) {
-                        m_use = m_tile;
-                    } else if (m_tile > m_run + 8.0f) {
-                        m_use = m_tile;
-                        rescale = true;
-                    }
-                }
-                if (__any_sync(0xffffffffu, rescale)) {
-                    // PV of this tile's previous step completed before S_n (in-order MMA).
-                    const float alpha = rescale ? fast_exp2(m_run - m_use) : 1.0f;
-                    l_run *= alpha;
-#pragma unroll
-                    for (int c = 0; c < D / 32; ++c) {
-                        uint32_t u[32];
-                        tmem_ld32(tO + c * 32, u);
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int chunk = hh ? s.c1 : s.c0;
+                    const uint32_t msk = t ? (hh ? s.b1 : s.b0) : (hh ? s.a1 : s.a0);
+                    if (chunk < 0 || !msk) continue;
+                    const uint32_t half = k_cnt & 1;  // S half of this chunk
+                    const uint32_t k_here = k_cnt++;
+                    if (r == 0) S2FTRACE(4 + 2 * t, s_cnt);
+                    mbar_wait(smem_u32(&bar_sf[t][half]), (k_here >> 1) & 1);
+                    if (r == 0) S2FTRACE(5 + 2 * t, s_cnt);
+                    ++s_cnt;
+                    tc_fence_after();
+                    float sv[64];
+                    {
+                        uint32_t* u = reinterpret_cast<uint32_t*>(sv);
+                        tmem_ld32(tS + half * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
+                        tmem_ld32(tS + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
                         tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            u[j] = __float_as_uint(__uint_as_float(u[j]) * alpha);
-                        tmem_st32(tO + c * 32, u);
                     }
-                }
-                m_run = m_use;
-                const float base = (m_use == -INFINITY) ? 0.f : m_use;
-                // P = 2^(S*scale*log2e - m): packed FFMA2, half of the pairs on MUFU.EX2 and
-                // half on the FMA pipe (exp2_poly2) so the XU pipe stops pacing the tile
-                const uint64_t sl2v = f2_pack(sl2, sl2), nbase = f2_pack(-base, -base);
-                uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};  // +0.0f pairs; 4 independent chains
+                    apply_mask(sv, chunk, msk, rg, q_pos, row0);
+                    float mxa[8];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    if (c < 2 || both) {
+                    for (int k = 0; k < 8; ++k) mxa[k] = fmaxf(sv[k], sv[k + 8]);
+#pragma unroll
+                    for (int j = 16; j < 64; j += 16)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) mxa[k] = fmaxf(mxa[k], fmaxf(sv[j + k], sv[j + k + 8]));
+                    const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                                           fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+                    const float m_tile = mx * sl2;
+                    float m_use = m_run;
+                    bool rescale = false;
+                    if (m_tile > m_run) {
+                        if (m_run == -INFINITY) {
+                            m_use = m_tile;
+                        } else if (m_tile > m_run + 8.0f) {
+                            m_use = m_tile;
+                            rescale = true;
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, rescale)) {
+                        // O must hold every earlier chunk's P V before it is rescaled: the
+                        // last one issued is this tile's chunk k_here-1 (its (k_here-1)-th
+                        // P V overall), still possibly in flight
+                        if (k_here > 0) mbar_wait(smem_u32(&bar_pv[t]), (k_here - 1) & 1);
+                        tc_fence_after();
+                        const float alpha = rescale ? fast_exp2(m_run - m_use) : 1.0f;
+                        l_run *= alpha;
+#pragma unroll
+                        for (int c = 0; c < D / 32; ++c) {
+                            uint32_t u[32];
+                            tmem_ld32(tO + c * 32, u);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) u[j] = __float_as_uint(__uint_as_float(u[j]) * alpha);
+                            tmem_st32(tO + c * 32, u);
+                        }
+                    }
+                    m_run = m_use;
+                    const float base = (m_use == -INFINITY) ? 0.f : m_use;
+                    const uint64_t sl2v = f2_pack(sl2, sl2), nbase = f2_pack(-base, -base);
+                    uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
                         uint32_t pk[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const uint64_t x = ffma2(f2_pack(sv[c * 32 + 2 * j], sv[c * 32 + 2 * j + 1]), sl2v, nbase);
                             uint64_t pr;
-                            if ((j & 1) == 1) {
+                            if ((j & 3) == 3) {
                                 pr = exp2_poly2(x);
                             } else {
                                 float x0, x1;
@@ -400,19 +402,17 @@ __global__ void __launch_bounds__(384, 1)
                             f2_unpack(pr, p0, p1);
                             pk[j] = pack_bf16(p0, p1);
                         }
-                        tmem_st16(tS + c * 16, pk);
+                        tmem_st16(tS + half * 64 + c * 16, pk);
                     }
+                    {
+                        float a0, a1;
+                        f2_unpack(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), a0, a1);
+                        l_run += a0 + a1;
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                    mbar_arrive(smem_u32(&bar_pf[t][half]));
                 }
-                float sum;
-                {
-                    float a0, a1;
-                    f2_unpack(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), a0, a1);
-                    sum = a0 + a1;
-                }
-                l_run += sum;
-                tmem_st_wait();
-                tc_fence_before();
-                mbar_arrive(smem_u32(&bar_pf[t]));
             }
             // ---------------------------------------------------- epilogue
             mbar_wait(smem_u32(&bar_of[t]), o_cnt & 1);
@@ -430,8 +430,7 @@ __global__ void __launch_bounds__(384, 1)
                     uint32_t* wp = reinterpret_cast<uint32_t*>(w);
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        wp[j] = pack_bf16(__uint_as_float(u[2 * j]) * inv_l,
-                                          __uint_as_float(u[2 * j + 1]) * inv_l);
+                        wp[j] = pack_bf16(__uint_as_float(u[2 * j]) * inv_l, __uint_as_float(u[2 * j + 1]) * inv_l);
                     uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) dst[j] = w[j];
