@@ -7,7 +7,10 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libs2attn.so")
+# S2ATTN_VARIANT=<name>: a kernel-tuning build from tools/build_variant.sh
+# (paper_2407_17678_b200/variants/<name>/libs2attn.so); unset in production
+LIB_PATH = os.path.join(HERE, *(("variants", os.environ["S2ATTN_VARIANT"]) if os.environ.get("S2ATTN_VARIANT") else ()),
+                        "libs2attn.so")
 
 S2_OK = 0
 S2_ERR_INVALID_ARGUMENT = 1

@@ -92,15 +92,21 @@ struct BwdCfg {
     static constexpr int kSub = D / 64;
     static constexpr int kTile128 = kSub * 16384;  // 128 rows x D bf16
     static constexpr int kTile64 = kSub * 8192;    // 64 rows x D bf16
-    // dkv: resident K, V (128 keys); kNSTkv stages of Q64, dO64 (1024-B aligned
-    // SW128 tiles); an aux slot per stage (lse2[64], delta[64], meta).
-    // The resident operands are double-buffered across items (the next
-    // item's load runs under this one) and a finished item's dead buffer is
-    // the staging tile of its epilogue's TMA stores.
-    static constexpr int kNSTkv = 3;
+    // dkv: resident K (128 keys) in 2 buffers (the next item's K loads under
+    // this item; a finished item's dead K tile stages its epilogue's TMA
+    // stores), V in 1 buffer (it is copied into TMEM at item start, so the
+    // next item's V can land right after); kNSTkv stages of Q64, dO64
+    // (1024-B aligned SW128 tiles), an aux slot per stage (lse2[64], delta[64],
+    // meta) and the barriers.  No static shared memory and no alignment slack:
+    // the dynamic window is declared 1024-B aligned (checked at run time).
+#ifndef S2_DKV_NST
+#define S2_DKV_NST 4
+#endif
+    static constexpr int kNSTkv = S2_DKV_NST;
     static constexpr int kDkvStage = 2 * kTile64;
     static constexpr int kAux = 528;
-    static constexpr int kDkvSmem = 1024 + 4 * kTile128 + kNSTkv * kDkvStage + kNSTkv * kAux;
+    static constexpr int kDkvBars = 256;
+    static constexpr int kDkvSmem = 3 * kTile128 + kNSTkv * kDkvStage + kNSTkv * kAux + kDkvBars;
     // dq: resident Q, dO (128 rows) in kQB buffers; kNSTq stages of K64, V64
 #ifndef S2_DQ_QBUF
 #define S2_DQ_QBUF 2
@@ -111,11 +117,11 @@ struct BwdCfg {
     static constexpr int kDqSmem = 1024 + kQB * 2 * kTile128 + kNSTq * kDqStage;
 };
 
-// Stage layout of the dK/dV kernel: Q rows [64][D] | dO rows [64][D] |
-// lse2[64] | delta[64] | meta (4 x u32: first q row, chunk-0 / chunk-1 masks of
-// this 64-row half (row groups 0..3), query data index).  The producer writes
-// meta with a plain shared store before its expect_tx arrive (release), so
-// whoever observes the stage's full barrier sees it: the MMA issuer and the
+// Stage layout of the dK/dV kernel: Q rows [64][D] | dO rows [64][D], and the
+// stage's aux slot: lse2[64] | delta[64] | meta (4 x u32: first q row, chunk-0 /
+// chunk-1 masks of this 64-row half (row groups 0..3), query data index).  The producer writes meta
+// with a plain shared store before its expect_tx arrive (release), so whoever
+// observes the stage's full barrier sees it: the MMA issuer and the
 // elementwise warps never touch the global entry list.
 template <int D>
 __global__ void __launch_bounds__(384, 1)
@@ -126,18 +132,34 @@ __global__ void __launch_bounds__(384, 1)
     using C = BwdCfg<D>;
     constexpr int NST = C::kNSTkv;
     constexpr int kMeta = 512;  // byte offset of the meta in a stage's aux slot
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    // bar_kve[kb]: K/V buffer kb is free (its item's last S^T/dP^T MMAs done AND both
-    // epilogue TMA stores, staged in it, have read it): count 3
-    __shared__ uint64_t bar_kvf[2], bar_kve[2], bar_sf[NST], bar_se[NST], bar_s[2], bar_p[2], bar_af, bar_ae;
-    __shared__ uint64_t bar_dpf;  // the elementwise warps have read dP^T (its single TMEM buffer is free)
-    __shared__ uint32_t tmem_base_s;
+    extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // K/V buffer kb: K at sK + kb * 2 * kTile128, V right after it
-    const uint32_t sK = smem_u32(smem), sV = sK + C::kTile128;
-    const uint32_t sSt = sK + 4 * C::kTile128;
+    if (tid == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1024-B alignment
+    // bar_kvf[kb]: K buffer kb and the V buffer hold the item's tiles.
+    // bar_kve[kb]: K buffer kb is free (its item's last S^T MMA done AND the
+    // epilogue TMA stores staged in it have read it): count 2.
+    // bar_ve: the item's V has been copied into TMEM (the V buffer is free).
+    // bar_dpf: the elementwise warps have read dP^T (its single TMEM buffer is free).
+    struct Bars {
+        uint64_t kvf[2], kve[2], ve, sf[NST], se[NST], s[2], p[2], af, ae, dpf;
+        uint32_t tmem_base;
+    };
+    static_assert(sizeof(Bars) <= C::kDkvBars, "barrier block");
+    Bars& bars = *reinterpret_cast<Bars*>(smem + 3 * C::kTile128 + NST * (C::kDkvStage + C::kAux));
+    auto& bar_kvf = bars.kvf;
+    auto& bar_kve = bars.kve;
+    auto& bar_ve = bars.ve;
+    auto& bar_sf = bars.sf;
+    auto& bar_se = bars.se;
+    auto& bar_s = bars.s;
+    auto& bar_p = bars.p;
+    auto& bar_af = bars.af;
+    auto& bar_ae = bars.ae;
+    auto& bar_dpf = bars.dpf;
+    auto& tmem_base_s = bars.tmem_base;
+    // K buffer kb at sK + kb * kTile128, the V buffer after both
+    const uint32_t sK = smem_u32(smem), sV = sK + 2 * C::kTile128;
+    const uint32_t sSt = sK + 3 * C::kTile128;
     const uint32_t sAux = sSt + NST * C::kDkvStage;
     uint8_t* const gAux = smem + (sAux - sK);  // generic pointer to aux 0
     const BwdItem* items = static_cast<const BwdItem*>(p.items);
@@ -146,8 +168,9 @@ __global__ void __launch_bounds__(384, 1)
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(smem_u32(&bar_kvf[i]), 1);
-            mbar_init(smem_u32(&bar_kve[i]), 3);
+            mbar_init(smem_u32(&bar_kve[i]), 2);
         }
+        mbar_init(smem_u32(&bar_ve), 1);
         mbar_init(smem_u32(&bar_af), 1);
         mbar_init(smem_u32(&bar_ae), 256);
         for (int i = 0; i < NST; ++i) {
@@ -191,13 +214,18 @@ __global__ void __launch_bounds__(384, 1)
                 const int kb = it_cnt & 1;
                 if (it_cnt >= 2) mbar_wait(smem_u32(&bar_kve[kb]), ((it_cnt >> 1) - 1) & 1);
                 const int nc = it.c1 >= 0 ? 2 : 1;
-                const uint32_t kvbar = smem_u32(&bar_kvf[kb]), kvoff = kb * 2 * C::kTile128;
+                const uint32_t kvbar = smem_u32(&bar_kvf[kb]), kvoff = kb * C::kTile128;
                 mbar_expect_tx(kvbar, 2 * nc * C::kSub * 8192);
                 for (int h = 0; h < nc; ++h)
                     for (int s = 0; s < C::kSub; ++s) {
                         const int row = (h ? it.c1 : it.c0) * 64;
                         tma_load_3d(sK + kvoff + s * 16384 + h * 8192, &tmK, kvbar, s * 64, row, it.kvbh);
-                        tma_load_3d(sV + kvoff + s * 16384 + h * 8192, &tmV, kvbar, s * 64, row, it.kvbh);
+                    }
+                if (it_cnt >= 1) mbar_wait(smem_u32(&bar_ve), (it_cnt - 1) & 1);
+                for (int h = 0; h < nc; ++h)
+                    for (int s = 0; s < C::kSub; ++s) {
+                        const int row = (h ? it.c1 : it.c0) * 64;
+                        tma_load_3d(sV + s * 16384 + h * 8192, &tmV, kvbar, s * 64, row, it.kvbh);
                     }
                 for (int j = 0; j < p.hpg; ++j) {
                     const int qbh = it.kvbh * p.hpg + j;
@@ -250,12 +278,13 @@ __global__ void __launch_bounds__(384, 1)
             for (int i = i_beg; i < i_end; ++i, ++it_cnt) {
                 const int nsteps = warp_uniform(items[i].nsteps);
                 const int kb = it_cnt & 1;
-                const uint32_t kvoff = (kb * 2 * C::kTile128) >> 4;
+                const uint32_t kvoff = (kb * C::kTile128) >> 4;
                 mbar_wait(smem_u32(&bar_kvf[kb]), (it_cnt >> 1) & 1);
                 if (leader) {  // V -> TMEM, after the previous item's last dP^T (issue order)
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk)
-                        tmem_cp_128x256b(tmem + kk * 8, dV0 + kvoff + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4));
+                        tmem_cp_128x256b(tmem + kk * 8, dV0 + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4));
+                    mma_commit(smem_u32(&bar_ve));  // the V buffer may be refilled
                 }
                 __syncwarp();
                 auto accumulate = [&](uint32_t n, int st, bool first) {
@@ -311,9 +340,8 @@ __global__ void __launch_bounds__(384, 1)
                             mma_ts(tmem + 192, tmem + kk * 8, dst + ((C::kTile64 >> 4) + bo), idS, kk > 0);
                         }
                         mma_commit(smem_u32(&bar_s[b]));
-                        // K / V are read by the S^T / dP^T MMAs only: release them after
-                        // the item's last ones so the next item's K / V load overlaps the
-                        // last dV / dK update and the epilogue.
+                        // K is read by the S^T MMAs only: release it after the item's
+                        // last ones (the epilogue stores staged in it arrive too).
                         if (s == nsteps - 1) mma_commit(smem_u32(&bar_kve[kb]));
                     }
                     __syncwarp();
@@ -421,57 +449,69 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
             // ---------------------------------------------------- epilogue
-            // TMEM -> registers (then the accumulators are released), bf16 into
-            // the swizzled staging tile, TMA stores (one 64 x 64 box per chunk
-            // and D/64 slice; rows past seq_len are clipped by the tensor map).
+            // TMEM -> registers (then the accumulators are released); dV, then dK,
+            // as bf16 into the swizzled staging tile over the item's dead K tile
+            // (warp group wg converts the row's 16-byte chunks [wg*D/16, (wg+1)*D/16)),
+            // TMA stores (one 64 x 64 box per chunk and D/64 slice; rows past seq_len
+            // are clipped by the tensor map).
             if (tid == 128) S2TRACE(8, it_cnt);
             mbar_wait(smem_u32(&bar_af), it_cnt & 1);
             if (tid == 128) S2TRACE(9, it_cnt);
             tc_fence_after();
-            const float mul = wg ? p.scale : 1.0f;  // wg0 -> dV, wg1 -> dK
-            uint32_t acc[D];
+            constexpr int kHalf = D / 2;  // columns per warp group (a multiple of 32)
+            uint32_t av[kHalf], ak[kHalf];
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c)
-                tmem_ld32(tmem + (wg ? 384 : 256) + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(acc + 32 * c));
+            for (int c = 0; c < kHalf / 32; ++c) {
+                tmem_ld32(tmem + 256 + wg * kHalf + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(av + 32 * c));
+                tmem_ld32(tmem + 384 + wg * kHalf + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(ak + 32 * c));
+            }
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(smem_u32(&bar_ae));
-            const bool wg_leader = (tid & 127) == 0;
+            const bool st_leader = tid == 128;
             if (release >= 0) {  // (an item without steps: release here at the latest)
                 bulk_wait_read0();
                 mbar_arrive(smem_u32(&bar_kve[release]));
                 release = -1;
             }
-            // bar_af: every MMA of the item is done, so its K/V buffer is dead: stage dV
-            // over its K tile (wg 0) and dK over its V tile (wg 1)
-            const uint32_t sOut = sK + (it_cnt & 1) * 2 * C::kTile128;
-            const uint32_t so = sOut + wg * C::kTile128 + hk * (C::kSub * 8192) + (kr & 63) * 128;
+            // bar_af: every MMA of the item is done, so its K tile is dead
+            const uint32_t sOut = sK + (it_cnt & 1) * C::kTile128;
+            const uint32_t so = sOut + hk * (C::kSub * 8192) + (kr & 63) * 128;
 #pragma unroll
-            for (int c = 0; c < D / 8; ++c) {  // 16-byte chunk c of the row: D/64 slice c>>3
-                const uint32_t w0 = pack_bf16(__uint_as_float(acc[8 * c]) * mul, __uint_as_float(acc[8 * c + 1]) * mul);
-                const uint32_t w1 = pack_bf16(__uint_as_float(acc[8 * c + 2]) * mul, __uint_as_float(acc[8 * c + 3]) * mul);
-                const uint32_t w2 = pack_bf16(__uint_as_float(acc[8 * c + 4]) * mul, __uint_as_float(acc[8 * c + 5]) * mul);
-                const uint32_t w3 = pack_bf16(__uint_as_float(acc[8 * c + 6]) * mul, __uint_as_float(acc[8 * c + 7]) * mul);
-                sts_u4(so + (c >> 3) * 8192 + (((c & 7) ^ (kr & 7)) << 4), w0, w1, w2, w3);
-            }
-            fence_proxy_async_smem();
-            named_bar_sync(1 + wg, 128);
-            if (wg_leader) {
-                const CUtensorMap* tm = wg ? &tmdK : &tmdV;
-                for (int h = 0; h < 2; ++h) {
-                    const int ch = h ? it.c1 : it.c0;
-                    if (ch < 0) continue;
-#pragma unroll
-                    for (int sb = 0; sb < C::kSub; ++sb)
-                        tma_store_3d(tm, sOut + wg * C::kTile128 + h * (C::kSub * 8192) + sb * 8192, sb * 64,
-                                     ch * 64, it.kvbh);
+            for (int ph = 0; ph < 2; ++ph) {  // 0: dV, 1: dK (scaled)
+                const uint32_t* acc = ph ? ak : av;
+                const float mul = ph ? p.scale : 1.0f;
+                if (ph == 1) {  // the dV stores must have read the staging tile
+                    if (st_leader) bulk_wait_read0();
+                    named_bar_sync(1, 256);
                 }
-                bulk_commit();
-                release = static_cast<int>(it_cnt & 1);  // arrive on bar_kve once the store has read it
+#pragma unroll
+                for (int j = 0; j < D / 16; ++j) {
+                    const int c = wg * (D / 16) + j;  // 16-byte chunk of the row: D/64 slice c>>3
+                    const uint32_t w0 = pack_bf16(__uint_as_float(acc[8 * j]) * mul, __uint_as_float(acc[8 * j + 1]) * mul);
+                    const uint32_t w1 = pack_bf16(__uint_as_float(acc[8 * j + 2]) * mul, __uint_as_float(acc[8 * j + 3]) * mul);
+                    const uint32_t w2 = pack_bf16(__uint_as_float(acc[8 * j + 4]) * mul, __uint_as_float(acc[8 * j + 5]) * mul);
+                    const uint32_t w3 = pack_bf16(__uint_as_float(acc[8 * j + 6]) * mul, __uint_as_float(acc[8 * j + 7]) * mul);
+                    sts_u4(so + (c >> 3) * 8192 + (((c & 7) ^ (kr & 7)) << 4), w0, w1, w2, w3);
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(1, 256);
+                if (st_leader) {
+                    const CUtensorMap* tm = ph ? &tmdK : &tmdV;
+                    for (int h = 0; h < 2; ++h) {
+                        const int ch = h ? it.c1 : it.c0;
+                        if (ch < 0) continue;
+#pragma unroll
+                        for (int sb = 0; sb < C::kSub; ++sb)
+                            tma_store_3d(tm, sOut + h * (C::kSub * 8192) + sb * 8192, sb * 64, ch * 64, it.kvbh);
+                    }
+                    bulk_commit();
+                }
             }
+            if (st_leader) release = static_cast<int>(it_cnt & 1);  // arrive on bar_kve once the stores have read it
             if (tid == 128) S2TRACE(10, it_cnt);
         }
-        if ((tid & 127) == 0) bulk_wait0();  // staging tiles must outlive the stores
+        if (tid == 128) bulk_wait0();  // staging tiles must outlive the stores
         (void)release;
     }
     tc_fence_before();
