@@ -107,14 +107,16 @@ struct BwdCfg {
     static constexpr int kAux = 528;
     static constexpr int kDkvBars = 256;
     static constexpr int kDkvSmem = 3 * kTile128 + kNSTkv * kDkvStage + kNSTkv * kAux + kDkvBars;
-    // dq: resident Q, dO (128 rows) in kQB buffers; kNSTq stages of K64, V64
-#ifndef S2_DQ_QBUF
-#define S2_DQ_QBUF 2
+    // dq: Q, dO (128 rows) in one buffer (they are copied into TMEM at item
+    // start, so the next item's tiles land right after), a dQ staging tile for
+    // the epilogue's TMA store, kNSTq stages of K64, V64 and the barriers.
+#ifndef S2_DQ_NST
+#define S2_DQ_NST 4
 #endif
-    static constexpr int kQB = S2_DQ_QBUF;
-    static constexpr int kNSTq = kQB == 2 ? 3 : 5;
+    static constexpr int kNSTq = S2_DQ_NST;
     static constexpr int kDqStage = 2 * kTile64;
-    static constexpr int kDqSmem = 1024 + kQB * 2 * kTile128 + kNSTq * kDqStage;
+    static constexpr int kDqBars = 256;
+    static constexpr int kDqSmem = 3 * kTile128 + kNSTq * kDqStage + kDqBars;
 };
 
 // Stage layout of the dK/dV kernel: Q rows [64][D] | dO rows [64][D], and the
@@ -530,25 +532,35 @@ __global__ void __launch_bounds__(384, 1)
                      const BwdParams p) {
     using C = BwdCfg<D>;
     constexpr int NST = C::kNSTq;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    // bar_qe[qb]: Q/dO buffer qb is free (last S/dP MMAs done AND the dQ TMA store,
-    // staged in its Q tile, has read it): count 2
-    __shared__ uint64_t bar_qf[2], bar_qe[2], bar_sf[NST], bar_se[NST], bar_s[2], bar_p[2], bar_af, bar_ae;
-    __shared__ uint32_t tmem_base_s;
+    extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // Q/dO buffer qb: Q at sQ + qb * 2 * kTile128, dO right after it
-    const uint32_t sQ = smem_u32(smem), sdO = sQ + C::kTile128;
-    const uint32_t sSt = sQ + C::kQB * 2 * C::kTile128;
+    if (tid == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1024-B alignment
+    // bar_qf / bar_qe: the Q/dO buffer holds the item's tiles / has been copied
+    // into TMEM (the buffer may be refilled)
+    struct Bars {
+        uint64_t qf, qe, sf[NST], se[NST], s[2], p[2], af, ae;
+        uint32_t tmem_base;
+    };
+    static_assert(sizeof(Bars) <= C::kDqBars, "barrier block");
+    Bars& bars = *reinterpret_cast<Bars*>(smem + 3 * C::kTile128 + NST * C::kDqStage);
+    auto& bar_qf = bars.qf;
+    auto& bar_qe = bars.qe;
+    auto& bar_sf = bars.sf;
+    auto& bar_se = bars.se;
+    auto& bar_s = bars.s;
+    auto& bar_p = bars.p;
+    auto& bar_af = bars.af;
+    auto& bar_ae = bars.ae;
+    auto& tmem_base_s = bars.tmem_base;
+    // Q at sQ, dO after it, the dQ staging tile after that, then the stages
+    const uint32_t sQ = smem_u32(smem), sdO = sQ + C::kTile128, sOut = sQ + 2 * C::kTile128;
+    const uint32_t sSt = sQ + 3 * C::kTile128;
     const FwdItem* items = static_cast<const FwdItem*>(p.items);
     const int2* chunks = static_cast<const int2*>(p.entries);
 
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(smem_u32(&bar_qf[i]), 1);
-            mbar_init(smem_u32(&bar_qe[i]), 2);
-        }
+        mbar_init(smem_u32(&bar_qf), 1);
+        mbar_init(smem_u32(&bar_qe), 1);
         mbar_init(smem_u32(&bar_af), 1);
         mbar_init(smem_u32(&bar_ae), 256);
         for (int i = 0; i < NST; ++i) {
@@ -585,13 +597,12 @@ __global__ void __launch_bounds__(384, 1)
             for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
                 const FwdItem it = items[i];
                 const int kvbh = it.bh / p.hpg;
-                const int qb = it_cnt % C::kQB;
-                if (it_cnt >= C::kQB) mbar_wait(smem_u32(&bar_qe[qb]), ((it_cnt / C::kQB) - 1) & 1);
-                const uint32_t qbar = smem_u32(&bar_qf[qb]), qoff = qb * 2 * C::kTile128;
+                if (it_cnt >= 1) mbar_wait(smem_u32(&bar_qe), (it_cnt - 1) & 1);
+                const uint32_t qbar = smem_u32(&bar_qf);
                 mbar_expect_tx(qbar, 2 * C::kTile128);
                 for (int s = 0; s < C::kSub; ++s) {
-                    tma_load_3d(sQ + qoff + s * 16384, &tmQ, qbar, s * 64, it.qtile * 128, it.bh);
-                    tma_load_3d(sdO + qoff + s * 16384, &tmdO, qbar, s * 64, it.qtile * 128, it.bh);
+                    tma_load_3d(sQ + s * 16384, &tmQ, qbar, s * 64, it.qtile * 128, it.bh);
+                    tma_load_3d(sdO + s * 16384, &tmdO, qbar, s * 64, it.qtile * 128, it.bh);
                 }
                 for (int n = 0; n < it.chunk_cnt; ++n, ++st_it) {
                     const int st = st_it % NST;
@@ -618,20 +629,16 @@ __global__ void __launch_bounds__(384, 1)
             const int i_end = p.sched[blockIdx.x + 1];
             for (int i = p.sched[blockIdx.x]; i < i_end; ++i, ++it_cnt) {
                 const int chunk_cnt = warp_uniform(items[i].chunk_cnt);
-                const int qb = it_cnt % C::kQB;
-                const uint32_t qoff = (qb * 2 * C::kTile128) >> 4;
-                mbar_wait(smem_u32(&bar_qf[qb]), (it_cnt / C::kQB) & 1);
+                mbar_wait(smem_u32(&bar_qf), it_cnt & 1);
                 if (leader) {  // after the previous item's last S / dP MMAs (issue order)
-                    const uint64_t dq0 = dQ0 + qoff, ddo0 = ddO0 + qoff;
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
                         const uint32_t ao = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-                        tmem_cp_128x256b(tmem + kk * 8, dq0 + ao);
-                        tmem_cp_128x256b(tmem + 64 + kk * 8, ddo0 + ao);
+                        tmem_cp_128x256b(tmem + kk * 8, dQ0 + ao);
+                        tmem_cp_128x256b(tmem + 64 + kk * 8, ddO0 + ao);
                     }
-                    // Q / dO now live in TMEM: the smem buffer may be refilled once the
-                    // copies are done (and the epilogue staged in it has been stored)
-                    mma_commit(smem_u32(&bar_qe[qb]));
+                    // Q / dO now live in TMEM: the buffer may be refilled once the copies are done
+                    mma_commit(smem_u32(&bar_qe));
                 }
                 __syncwarp();
                 bool first = true;
@@ -693,7 +700,6 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const float sl2 = p.scale_log2;
         uint32_t it_cnt = 0, n_glob = 0;
-        int release = -1;  // leader: Q/dO buffer whose dQ store is still in flight
         for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
             const FwdItem it = items[i];
             const int q_pos = it.qtile * 128 + r;
@@ -743,11 +749,6 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_before();
                 mbar_arrive(smem_u32(&bar_p[b]));
                 if (tid == 128) S2TRACE(7, n_glob);
-                if (release >= 0) {  // the previous item's store read its staging long ago
-                    bulk_wait_read0();
-                    mbar_arrive(smem_u32(&bar_qe[release]));
-                    release = -1;
-                }
             }
             mbar_wait(smem_u32(&bar_af), it_cnt & 1);
             tc_fence_after();
@@ -761,13 +762,9 @@ __global__ void __launch_bounds__(384, 1)
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(smem_u32(&bar_ae));
-            if (release >= 0) {  // (an item without chunks: release here at the latest)
-                bulk_wait_read0();
-                mbar_arrive(smem_u32(&bar_qe[release]));
-                release = -1;
-            }
-            // bar_af: every MMA of the item is done, so its Q tile is dead: stage dQ there
-            const uint32_t sOut = sQ + (it_cnt % C::kQB) * 2 * C::kTile128;
+            // the previous item's store has read the staging tile (long ago)
+            if (tid == 128) bulk_wait_read0();
+            named_bar_sync(1, 256);
             const float sc = it.chunk_cnt > 0 ? p.scale : 0.f;  // no chunks: dQ = 0
 #pragma unroll
             for (int c = 0; c < D / 16; ++c) {  // my 16-byte chunks: global chunk index g
@@ -785,16 +782,9 @@ __global__ void __launch_bounds__(384, 1)
                 for (int sb = 0; sb < C::kSub; ++sb)
                     tma_store_3d(&tmdQ, sOut + sb * 16384, sb * 64, it.qtile * 128, it.bh);
                 bulk_commit();
-                if (C::kQB == 1) {  // the next item's Q load waits on this buffer: release now
-                    bulk_wait_read0();
-                    mbar_arrive(smem_u32(&bar_qe[0]));
-                } else {
-                    release = static_cast<int>(it_cnt % C::kQB);  // arrive on bar_qe once the store has read it
-                }
             }
         }
         if (tid == 128) bulk_wait0();  // the staging tile must outlive the store
-        (void)release;
     }
     tc_fence_before();
     __syncthreads();
