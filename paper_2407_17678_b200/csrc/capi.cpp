@@ -15,7 +15,7 @@
 #include "tma_host.hpp"
 
 cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtensorMap& k,
-                                const CUtensorMap& v, const void* items, const int* sched,
+                                const CUtensorMap& v, const CUtensorMap& o, const void* items, const int* sched,
                                 int grid, const void* steps, __nv_bfloat16* out, float* lse,
                                 int seq_len, int hpg, float scale_log2, cudaStream_t stream);
 cudaError_t s2_launch_fwd_simt(bool bf16, const void* q, const void* k, const void* v, void* out,
@@ -674,8 +674,9 @@ int s2_attn_fwd(s2_plan* p, const s2_attn_args* a, s2_stream_t stream) {
             const CUtensorMap mq = s2host::make_map_bf16_3d(a->q, D, N, uint64_t(nu) * hpg, 64, 128);
             const CUtensorMap mk = s2host::make_map_bf16_3d(a->k, D, N, nu, 64, 64);
             const CUtensorMap mv = s2host::make_map_bf16_3d(a->v, D, N, nu, 64, 64);
+            const CUtensorMap mo = s2host::make_map_bf16_3d(a->out, D, N, uint64_t(nu) * hpg, 64, 128);
             ProfScope prof("fwd_sm100", st);
-            e = s2_launch_fwd_sm100(a->head_dim, mq, mk, mv, w->pair.ptr, w->pair_sched.as<int>(),
+            e = s2_launch_fwd_sm100(a->head_dim, mq, mk, mv, mo, w->pair.ptr, w->pair_sched.as<int>(),
                                     w->grid, L->d_steps.ptr, static_cast<__nv_bfloat16*>(a->out),
                                     a->lse, a->seq_len, hpg, float(scale * M_LOG2E), st);
         } catch (const std::exception& ex) {

@@ -67,9 +67,14 @@ struct Fwd2Cfg {
     static constexpr int kSub = D / 64;
     static constexpr int kQBytes = kSub * 16384;  // 128 rows
     static constexpr int kCBytes = kSub * 8192;   // one 64-key chunk of K (or V)
-    static constexpr int kNST = D == 128 ? 4 : 8;
+#ifndef S2_FWD_NST
+#define S2_FWD_NST 4
+#endif
+    static constexpr int kNST = D == 128 ? S2_FWD_NST : 8;
     static constexpr int kStageBytes = 2 * kCBytes;
-    static constexpr int kSmem = 1024 + 2 * kQBytes + kNST * kStageBytes;
+    // per tile, a 128-row x 64-column bf16 staging slice for the O epilogue's TMA stores
+    static constexpr int kStgBytes = 16384;
+    static constexpr int kSmem = 1024 + 2 * kQBytes + kNST * kStageBytes + 2 * kStgBytes;
 };
 
 __device__ __forceinline__ void apply_mask(float* s, int chunk, uint32_t mask, int rg, int q_pos,
@@ -92,7 +97,8 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     s2_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                         const __grid_constant__ CUtensorMap tmK,
-                        const __grid_constant__ CUtensorMap tmV, const Fwd2Params p) {
+                        const __grid_constant__ CUtensorMap tmV,
+                        const __grid_constant__ CUtensorMap tmO, const Fwd2Params p) {
     using C = Fwd2Cfg<D>;
     constexpr int NST = C::kNST;
     extern __shared__ uint8_t smem_raw[];
@@ -110,6 +116,7 @@ __global__ void __launch_bounds__(384, 1)
     const int warp = tid >> 5, lane = tid & 31;
     const uint32_t sQ0 = smem_u32(smem);
     const uint32_t sKV = sQ0 + 2 * C::kQBytes;
+    const uint32_t sStg = sKV + NST * C::kStageBytes;
 
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -205,7 +212,9 @@ __global__ void __launch_bounds__(384, 1)
                 int prev_st = -1;             // stage of the previous chunk (released after its P Vs)
                 auto issue_pv = [&](int t) {
                     const uint32_t tS = tmem + t * 256, tO = tS + 128;
+                    S2FTRACE(3 + 10 * t, p_cnt[t]);
                     mbar_wait(smem_u32(&bar_pf[t][p_cnt[t] & 1]), (p_cnt[t] >> 1) & 1);
+                    S2FTRACE(12 + 2 * t, p_cnt[t]);
                     ++p_cnt[t];
                     if (first_pv[t] && o_use[t] > 0) mbar_wait(smem_u32(&bar_oe[t]), (o_use[t] - 1) & 1);
                     tc_fence_after();  // P was written to TMEM by tcgen05.st
@@ -230,7 +239,9 @@ __global__ void __launch_bounds__(384, 1)
                         if (chunk < 0) continue;
                         const uint32_t mk[2] = {warp_uniform(h ? ps.a1 : ps.a0), warp_uniform(h ? ps.b1 : ps.b0)};
                         const int st = kv_it % NST;
+                        S2FTRACE(0, kv_it);
                         mbar_wait(smem_u32(&bar_kf[st]), (kv_it / NST) & 1);
+                        S2FTRACE(1, kv_it);
                         const uint64_t dk = dKV0 + static_cast<uint64_t>((st * C::kStageBytes) >> 4);
                         // S_t(j) for both tiles first: they run while P_t(j-1) is computed
                         uint32_t s_half[2] = {0, 0};
@@ -252,6 +263,7 @@ __global__ void __launch_bounds__(384, 1)
                             }
                             __syncwarp();
                         }
+                        S2FTRACE(2, kv_it);
                         // then the pending P V of each tile (chunk j-1 or earlier)
 #pragma unroll
                         for (int t = 0; t < 2; ++t)
@@ -280,20 +292,25 @@ __global__ void __launch_bounds__(384, 1)
                         ++kv_it;
                     }
                 }
+                // every S of the item is issued: the Q tiles are free once they complete
+                // (the next item's Q loads overlap the last softmax, P V and epilogue)
+                if (leader)
+                    for (int t = 0; t < 2; ++t)
+                        if (has[t]) mma_commit(smem_u32(&bar_qe[t]));
+                __syncwarp();
+                // each tile's O is final after its own last P V (no wait on the other tile)
 #pragma unroll
-                for (int t = 0; t < 2; ++t)
+                for (int t = 0; t < 2; ++t) {
                     if (pend_st[t] >= 0) issue_pv(t);
+                    if (has[t]) {
+                        if (leader) mma_commit(smem_u32(&bar_of[t]));
+                        __syncwarp();
+                    }
+                }
                 if (prev_st >= 0) {
                     if (leader) mma_commit(smem_u32(&bar_ke[prev_st]));
                     __syncwarp();
                 }
-                if (leader)
-                    for (int t = 0; t < 2; ++t)
-                        if (has[t]) {
-                            mma_commit(smem_u32(&bar_of[t]));
-                            mma_commit(smem_u32(&bar_qe[t]));
-                        }
-                __syncwarp();
                 for (int t = 0; t < 2; ++t)
                     if (has[t]) {
                         ++o_use[t];
@@ -412,37 +429,52 @@ __global__ void __launch_bounds__(384, 1)
                     tmem_st_wait();
                     tc_fence_before();
                     mbar_arrive(smem_u32(&bar_pf[t][half]));
+                    if (r == 0 && t == 0) S2FTRACE(8, s_cnt - 1);
                 }
             }
             // ---------------------------------------------------- epilogue
+            // O -> registers (then its TMEM is released to the next item), x 1/l as
+            // bf16 into this tile's swizzled staging slice, one TMA store per 64
+            // columns (rows past seq_len are clipped by the tensor map)
+            if (r == 0 && t == 0) S2FTRACE(9, o_cnt);
             mbar_wait(smem_u32(&bar_of[t]), o_cnt & 1);
+            if (r == 0 && t == 0) S2FTRACE(10, o_cnt);
             tc_fence_after();
-            const float inv_l = 1.0f / l_run;
-            const bool valid = q_pos < p.seq_len;
-            __nv_bfloat16* orow = p.out + (static_cast<size_t>(it.bh) * p.seq_len + q_pos) * D;
+            uint32_t ov[D];
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                uint32_t u[32];
-                tmem_ld32(tO + c * 32, u);
-                tmem_ld_wait();
-                if (valid) {
-                    uint4 w[4];
-                    uint32_t* wp = reinterpret_cast<uint32_t*>(w);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        wp[j] = pack_bf16(__uint_as_float(u[2 * j]) * inv_l, __uint_as_float(u[2 * j + 1]) * inv_l);
-                    uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) dst[j] = w[j];
-                }
-            }
-            if (valid)
-                p.lse[static_cast<size_t>(it.bh) * p.seq_len + q_pos] =
-                    (m_run + __log2f(l_run)) * 0.69314718055994530942f;
+            for (int c = 0; c < D / 32; ++c) tmem_ld32(tO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(ov + 32 * c));
+            tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(smem_u32(&bar_oe[t]));
+            const float inv_l = 1.0f / l_run;
+            const uint32_t stg = sStg + t * C::kStgBytes;
+#pragma unroll
+            for (int j = 0; j < D / 64; ++j) {
+                if (r == 0) bulk_wait_read0();  // the previous store has read the slice
+                named_bar_sync(1 + t, 128);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const uint32_t* u = ov + j * 64 + c * 8;
+                    sts_u4(stg + r * 128 + ((c ^ (r & 7)) << 4),
+                           pack_bf16(__uint_as_float(u[0]) * inv_l, __uint_as_float(u[1]) * inv_l),
+                           pack_bf16(__uint_as_float(u[2]) * inv_l, __uint_as_float(u[3]) * inv_l),
+                           pack_bf16(__uint_as_float(u[4]) * inv_l, __uint_as_float(u[5]) * inv_l),
+                           pack_bf16(__uint_as_float(u[6]) * inv_l, __uint_as_float(u[7]) * inv_l));
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(1 + t, 128);
+                if (r == 0) {
+                    tma_store_3d(&tmO, stg, j * 64, row0, it.bh);
+                    bulk_commit();
+                }
+            }
+            if (q_pos < p.seq_len)
+                p.lse[static_cast<size_t>(it.bh) * p.seq_len + q_pos] =
+                    (m_run + __log2f(l_run)) * 0.69314718055994530942f;
+            if (r == 0 && t == 0) S2FTRACE(11, o_cnt);
             ++o_cnt;
         }
+        if (r == 0) bulk_wait0();  // the staging slice must outlive the stores
     }
     tc_fence_before();
     __syncthreads();
@@ -454,12 +486,12 @@ __global__ void __launch_bounds__(384, 1)
 
 template <int D>
 static cudaError_t launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                          const Fwd2Params& p, int grid, cudaStream_t stream) {
+                          const CUtensorMap& o, const Fwd2Params& p, int grid, cudaStream_t stream) {
     auto kern = s2_fwd_sm100_kernel<D>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::kSmem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 384, Fwd2Cfg<D>::kSmem, stream>>>(q, k, v, p);
+    kern<<<grid, 384, Fwd2Cfg<D>::kSmem, stream>>>(q, k, v, o, p);
     return cudaGetLastError();
 }
 
@@ -468,14 +500,14 @@ static cudaError_t launch(const CUtensorMap& q, const CUtensorMap& k, const CUte
 // Host entry used by capi.cpp: items grouped per CTA, sched = [grid + 1] offsets.
 long long* s2_debug_trace_buffer();
 cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtensorMap& k,
-                                const CUtensorMap& v, const void* items, const int* sched,
+                                const CUtensorMap& v, const CUtensorMap& o, const void* items, const int* sched,
                                 int grid, const void* steps, __nv_bfloat16* out, float* lse,
                                 int seq_len, int hpg, float scale_log2, cudaStream_t stream) {
     if (grid == 0) return cudaSuccess;
     s2dev::Fwd2Params p{static_cast<const s2dev::PairItem*>(items), sched,
                         static_cast<const s2dev::PairStep*>(steps), out, lse, seq_len, hpg,
                         scale_log2, s2_debug_trace_buffer()};
-    if (head_dim == 128) return s2dev::launch<128>(q, k, v, p, grid, stream);
-    if (head_dim == 64) return s2dev::launch<64>(q, k, v, p, grid, stream);
+    if (head_dim == 128) return s2dev::launch<128>(q, k, v, o, p, grid, stream);
+    if (head_dim == 64) return s2dev::launch<64>(q, k, v, o, p, grid, stream);
     return cudaErrorInvalidValue;
 }

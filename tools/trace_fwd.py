@@ -28,7 +28,29 @@ print("tile-0 softmax steps traced", n)
 print("softmax0: wait S", m(t[5, lo:hi] - t[4, lo:hi]), " step period", m(np.diff(t[5, lo:hi])))
 print("softmax0: S ok -> next wait (compute+store+arrive)", m(t[4, lo + 1:hi + 1] - t[5, lo:hi]))
 print("softmax1: wait S", m(t[7, lo:hi] - t[6, lo:hi]), " compute", m(t[6, lo + 1:hi + 1] - t[7, lo:hi]))
-print("MMA: wait P0", m(t[1, lo:hi] - t[0, lo:hi]), " wait K", m(t[3, lo:hi] - t[2, lo:hi]))
+print("softmax0: S ok -> P arrive", m(t[8, lo:hi] - t[5, lo:hi]), " P arrive -> next wait", m(t[4, lo + 1:hi + 1] - t[8, lo:hi]))
+nk = int((t[2] > 0).sum())
+if nk > 40:
+    a, b = 20, min(nk, 1500)
+    print(f"MMA: chunks {nk}: wait K {m(t[1, a:b] - t[0, a:b]):.0f}, S issue {m(t[2, a:b] - t[1, a:b]):.0f}, "
+          f"S issued -> next chunk {m(t[0, a + 1:b + 1] - t[2, a:b]):.0f}, chunk period {m(np.diff(t[0, a:b])):.0f}")
+    print(f"MMA: wait P tile0 {m(t[12, a:b] - t[3, a:b]):.0f}, wait P tile1 {m(t[14, a:b] - t[13, a:b]):.0f}")
+    wk = (t[1, a:b] - t[0, a:b]).astype(np.float64).sum()
+    wp = ((t[12, a:b] - t[3, a:b]) + (t[14, a:b] - t[13, a:b])).astype(np.float64).sum()
+    span = float(t[0, b] - t[0, a])
+    print(f"MMA warp share: wait K {wk / span:.1%}, wait P {wp / span:.1%}")
+ni = int((t[11] > 0).sum())
+if ni > 3:
+    e = slice(1, ni - 1)
+    tot = float(t[11, ni - 1] - t[9, 0])
+    ep = (t[11, e] - t[10, e]).astype(np.float64)
+    wo = (t[10, e] - t[9, e]).astype(np.float64)
+    print(f"items {ni}: epilogue median {np.median(ep):.0f} cycles, wait O {np.median(wo):.0f}; "
+          f"epilogue+wait share of CTA-0 time {(ep.sum() + wo.sum()) / tot:.1%}")
+    busy = (t[8, lo:hi] - t[5, lo:hi]).astype(np.float64).sum()
+    waits = (t[5, lo:hi] - t[4, lo:hi]).astype(np.float64).sum()
+    span = float(t[8, hi - 1] - t[4, lo])
+    print(f"softmax0 over steps {lo}..{hi}: compute {busy / span:.1%}, wait S {waits / span:.1%}, other {1 - (busy + waits) / span:.1%}")
 if (t[12] > 0).sum() > 10:  # built with -DS2_FWD_DETAIL_TRACE
     k = np.arange(lo, hi)
     names = ["S ok -> ld done", "mask + local max", "max exchange", "exp + P store", "rescale + st wait + arrive"]
