@@ -16,9 +16,13 @@ ap.add_argument("--d", type=int, default=128)
 ap.add_argument("--v", type=int, default=16)
 ap.add_argument("--local", type=int, default=4)
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--uniform", action="store_true", help="U[-1,1] inputs (bench.py's data) instead of N(0,1)")
 a = ap.parse_args()
 plan = s2.Plan.from_config(s2.make_s2_config(a.n, a.h, local_blocks=a.local, vert_stride=a.v))
-mk = lambda: torch.randn(a.b, a.h, a.n, a.d, device="cuda", dtype=torch.bfloat16)  # noqa
+if a.uniform:
+    mk = lambda: (torch.rand(a.b, a.h, a.n, a.d, device="cuda") * 2 - 1).to(torch.bfloat16)  # noqa
+else:
+    mk = lambda: torch.randn(a.b, a.h, a.n, a.d, device="cuda", dtype=torch.bfloat16)  # noqa
 q, k, v, do = mk(), mk(), mk(), mk()
 out, lse = s2.s2_attn_fwd(plan, q, k, v)
 dq, dk, dv = s2.s2_attn_bwd(plan, q, k, v, out, lse, do)
