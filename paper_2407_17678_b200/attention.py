@@ -235,37 +235,13 @@ def s2_attn_fwd_bwd_host(plan: Plan, q, k, v, dout, out, lse, dq, dk, dv, *,
     return workspace
 
 
-def _autograd_fn():
-    import torch
-
-    class _S2Attention(torch.autograd.Function):
-        @staticmethod
-        def forward(ctx, q, k, v, plan, scale):
-            out, lse = s2_attn_fwd(plan, q.contiguous(), k.contiguous(), v.contiguous(),
-                                   scale=scale)
-            ctx.save_for_backward(q, k, v, out, lse)
-            ctx.plan, ctx.scale = plan, scale
-            return out
-
-        @staticmethod
-        def backward(ctx, dout):
-            q, k, v, out, lse = ctx.saved_tensors
-            dq, dk, dv = s2_attn_bwd(ctx.plan, q, k, v, out, lse, dout.contiguous(),
-                                     scale=ctx.scale)
-            return dq, dk, dv, None, None
-
-    return _S2Attention
-
-
-_FN = None
-
-
 def s2_attention(q, k, v, plan: Plan, scale: Optional[float] = None):
-    """Differentiable S2 attention (DKernel's plug-in role)."""
-    global _FN
-    if _FN is None:
-        _FN = _autograd_fn()
-    return _FN.apply(q, k, v, plan, scale)
+    """Differentiable S2 attention (DKernel's plug-in role): the
+    `s2attn::fwd` torch.library op, whose registered autograd formula calls
+    `s2attn::bwd` (torch_ops.py)."""
+    from .torch_ops import s2_attention as op
+
+    return op(q, k, v, plan, scale)
 
 
 # ----------------------------------------------------- reference-shaped API
