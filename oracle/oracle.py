@@ -74,6 +74,9 @@ def port():
                                                          _IP, _F, _F, _F]),
             "s2o_decode": (None, [ctypes.c_int] * 7 + [ctypes.c_double, _F, _F, _F,
                                                        _IP, _IP, ctypes.c_int, _F, _D]),
+            "s2o_bwd_sample": (None, [ctypes.c_int] * 6 + [ctypes.c_double, _F, _F, _F, _F, _IP, _IP,
+                                                           ctypes.c_int, _IP, _F, ctypes.c_int, _IP,
+                                                           _F, _F]),
             "s2o_max_rel_f": (ctypes.c_double, [_F, _F, ctypes.c_int64]),
             "s2o_max_rel_d": (ctypes.c_double, [_D, _D, ctypes.c_int64]),
         }
@@ -203,6 +206,25 @@ def decode(q, k, v, row_ptr, col_idx, batch, H, Hkv, T, D, S, t, B, scale=None):
                       ip(np.ascontiguousarray(row_ptr, np.int32)),
                       ip(np.ascontiguousarray(col_idx, np.int32)), B, fp(out), dp(lse))
     return out, lse
+
+
+def bwd_sample(q, k, v, dout, row_ptr, col_idx, batch, H, Hkv, N, D, S, q_rows, k_rows,
+               scale=None):
+    """s2o_attn_bwd's gradient at sampled rows (s2o_bwd_sample), for full-size
+    parity: q_rows = [(b*H + h, i)] -> dq rows; k_rows = [(b*Hkv + g, j)] ->
+    (dk, dv) rows.  q/dout [batch,H,N,D], k/v [batch,Hkv,N,D] fp32 (flat ok)."""
+    scale = 1.0 / np.sqrt(D) if scale is None else scale
+    q, k, v, dout = (np.ascontiguousarray(x, np.float32) for x in (q, k, v, dout))
+    qs = np.ascontiguousarray(np.asarray(q_rows, np.int32).reshape(-1, 2))
+    ks = np.ascontiguousarray(np.asarray(k_rows, np.int32).reshape(-1, 2))
+    dq = np.zeros((len(qs), D), np.float32)
+    dk = np.zeros((len(ks), D), np.float32)
+    dv = np.zeros((len(ks), D), np.float32)
+    port().s2o_bwd_sample(batch, H, Hkv, N, D, S, scale, fp(q), fp(k), fp(v), fp(dout),
+                          ip(np.ascontiguousarray(row_ptr, np.int32)),
+                          ip(np.ascontiguousarray(col_idx, np.int32)), len(qs), ip(qs), fp(dq),
+                          len(ks), ip(ks), fp(dk), fp(dv))
+    return dq, dk, dv
 
 
 def max_rel(a, b):

@@ -420,6 +420,147 @@ void s2o_attn_bwd(int batch, int H, int Hkv, int N, int D, int S, double scale, 
     free(col_off);
 }
 
+/* ------------------------------------------------- sampled backward rows */
+
+/* Row statistics of query row i (reference.cpp:28-45 two-pass): max m, sum z
+ * of exp(scale*q_i.k_j - m) over the admitted keys, and delta = dO_i . O_i. */
+static void row_stats(const float* qi, const float* doi, const float* K, const float* V,
+                      const int* rp, const int* ci, int i, int S, int D, double scale,
+                      double* m_out, double* z_out, double* delta_out) {
+    const int bi = i / S;
+    double mx = -INFINITY;
+    for (int ptr = rp[bi]; ptr < rp[bi + 1]; ++ptr)
+        for (int j = ci[ptr] * S; j < ci[ptr] * S + S && j <= i; ++j) {
+            double dot = 0.0;
+            for (int x = 0; x < D; ++x) dot += (double)qi[x] * K[(size_t)j * D + x];
+            if (scale * dot > mx) mx = scale * dot;
+        }
+    double z = 0.0, dl = 0.0;
+    for (int ptr = rp[bi]; ptr < rp[bi + 1]; ++ptr)
+        for (int j = ci[ptr] * S; j < ci[ptr] * S + S && j <= i; ++j) {
+            double dot = 0.0, dp = 0.0;
+            for (int x = 0; x < D; ++x) {
+                dot += (double)qi[x] * K[(size_t)j * D + x];
+                dp += (double)doi[x] * V[(size_t)j * D + x];
+            }
+            const double w = exp(scale * dot - mx);
+            z += w;
+            dl += w * dp;  /* sum_j p_ij (dO_i . v_j) * z  ==  z * (dO_i . O_i) */
+        }
+    *m_out = mx;
+    *z_out = z;
+    *delta_out = dl / z;
+}
+
+/* Does row block bi list key block bj?  (CSR rows are strictly ascending) */
+static int row_has_block(const int* rp, const int* ci, int bi, int bj) {
+    int lo = rp[bi], hi = rp[bi + 1];
+    while (lo < hi) {
+        const int mid = (lo + hi) / 2;
+        if (ci[mid] < bj) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < rp[bi + 1] && ci[lo] == bj;
+}
+
+/* The gradient of s2o_attn_bwd at sampled rows, for full-size parity checks
+ * (it is the same definition: p_ij = exp(scale q_i.k_j - m_i)/z_i over the
+ * admitted set, dS_ij = p_ij (dO_i.v_j - delta_i)):
+ *   qsel[2n] = (u = b*H + h, i)    -> dq_out[n*D]  = scale * sum_j dS_ij k_j
+ *   ksel[2n] = (g = b*Hkv + kv, j) -> dk_out[n*D]  = scale * sum_{h in group, i} dS_ij q_i
+ *                                     dv_out[n*D]  = sum_{h in group, i} p_ij dO_i
+ * Key rows visit every admitted query row of the group's heads (rows whose
+ * block row lists j's block, i >= j), in parallel over i. */
+void s2o_bwd_sample(int batch, int H, int Hkv, int N, int D, int S, double scale, const float* q,
+                    const float* k, const float* v, const float* dout, const int* row_ptr,
+                    const int* col_idx, int nq, const int* qsel, float* dq_out, int nk,
+                    const int* ksel, float* dk_out, float* dv_out) {
+    const int B = (N + S - 1) / S;
+    const int hpg = H / Hkv;
+    (void)batch;  /* rows are addressed by their (batch, head) unit index */
+    int64_t* col_off = (int64_t*)malloc(sizeof(int64_t) * (size_t)H);
+    head_offsets(H, B, row_ptr, col_off);
+#pragma omp parallel for schedule(dynamic)
+    for (int n = 0; n < nq; ++n) {
+        const int u = qsel[2 * n], i = qsel[2 * n + 1];
+        const int b = u / H, h = u % H, bi = i / S;
+        const size_t qo = (size_t)u * N * D;
+        const float* qi = q + qo + (size_t)i * D;
+        const float* doi = dout + qo + (size_t)i * D;
+        const float* K = k + ((size_t)b * Hkv + h / hpg) * (size_t)N * D;
+        const float* V = v + ((size_t)b * Hkv + h / hpg) * (size_t)N * D;
+        const int* rp = row_ptr + (size_t)h * (B + 1);
+        const int* ci = col_idx + col_off[h];
+        double mx, z, delta;
+        row_stats(qi, doi, K, V, rp, ci, i, S, D, scale, &mx, &z, &delta);
+        double* gq = (double*)calloc((size_t)D, sizeof(double));
+        for (int ptr = rp[bi]; ptr < rp[bi + 1]; ++ptr)
+            for (int j = ci[ptr] * S; j < ci[ptr] * S + S && j <= i; ++j) {
+                double dot = 0.0, dp = 0.0;
+                for (int x = 0; x < D; ++x) {
+                    dot += (double)qi[x] * K[(size_t)j * D + x];
+                    dp += (double)doi[x] * V[(size_t)j * D + x];
+                }
+                const double ds = exp(scale * dot - mx) / z * (dp - delta);
+                for (int x = 0; x < D; ++x) gq[x] += ds * K[(size_t)j * D + x];
+            }
+        for (int x = 0; x < D; ++x) dq_out[(size_t)n * D + x] = (float)(scale * gq[x]);
+        free(gq);
+    }
+    for (int n = 0; n < nk; ++n) {
+        const int g = ksel[2 * n], j = ksel[2 * n + 1];
+        const int b = g / Hkv, kv = g % Hkv, bj = j / S;
+        const float* K = k + (size_t)g * N * D;
+        const float* V = v + (size_t)g * N * D;
+        double* gk = (double*)calloc((size_t)D, sizeof(double));
+        double* gv = (double*)calloc((size_t)D, sizeof(double));
+        for (int hh = 0; hh < hpg; ++hh) {
+            const int h = kv * hpg + hh;
+            const size_t qo = ((size_t)b * H + h) * N * D;
+            const int* rp = row_ptr + (size_t)h * (B + 1);
+            const int* ci = col_idx + col_off[h];
+#pragma omp parallel
+            {
+                double* lk = (double*)calloc((size_t)D, sizeof(double));
+                double* lv = (double*)calloc((size_t)D, sizeof(double));
+#pragma omp for schedule(dynamic, 64)
+                for (int i = j; i < N; ++i) {
+                    if (!row_has_block(rp, ci, i / S, bj)) continue;
+                    const float* qi = q + qo + (size_t)i * D;
+                    const float* doi = dout + qo + (size_t)i * D;
+                    double mx, z, delta;
+                    row_stats(qi, doi, K, V, rp, ci, i, S, D, scale, &mx, &z, &delta);
+                    double dot = 0.0, dp = 0.0;
+                    for (int x = 0; x < D; ++x) {
+                        dot += (double)qi[x] * K[(size_t)j * D + x];
+                        dp += (double)doi[x] * V[(size_t)j * D + x];
+                    }
+                    const double pij = exp(scale * dot - mx) / z;
+                    const double ds = pij * (dp - delta);
+                    for (int x = 0; x < D; ++x) {
+                        lk[x] += ds * qi[x];
+                        lv[x] += pij * doi[x];
+                    }
+                }
+#pragma omp critical
+                for (int x = 0; x < D; ++x) {
+                    gk[x] += lk[x];
+                    gv[x] += lv[x];
+                }
+                free(lk);
+                free(lv);
+            }
+        }
+        for (int x = 0; x < D; ++x) {
+            dk_out[(size_t)n * D + x] = (float)(scale * gk[x]);
+            dv_out[(size_t)n * D + x] = (float)gv[x];
+        }
+        free(gk);
+        free(gv);
+    }
+    free(col_off);
+}
+
 /* -------------------------------------------------------------- decode */
 
 /* Single query row at position t for every (batch, head): the row form of

@@ -203,3 +203,28 @@ def test_port_decode_equals_forward_row():
         o, l = oracle.decode(qt, k, v, rp, ci, 1, H, Hkv, N, d, S, t, cfg.num_blocks())
         np.testing.assert_allclose(o, out.reshape(H, N, d)[:, t].ravel(), rtol=1e-6, atol=1e-7)
         np.testing.assert_allclose(l, lse.reshape(H, N)[:, t], rtol=1e-12)
+
+
+@pytest.mark.parametrize("case", ["gqa_ragged", "batch2"])
+def test_port_sampled_backward_rows_equal_full_backward(case):
+    """s2o_bwd_sample (the full-size parity checker) restates s2o_attn_bwd at
+    sampled rows: pinned against the full port backward on small cases."""
+    if case == "gqa_ragged":
+        cfg, batch, D = single(300, 16, 4, 2, 3, kv=2), 1, 32
+    else:
+        cfg, batch, D = single(256, 32, 2, 1, 2), 2, 16
+    H, Hkv, N, S = cfg.num_heads, cfg.kv_heads(), cfg.seq_len, cfg.block_size
+    rng = np.random.default_rng(11)
+    q, do = (rng.uniform(-1, 1, batch * H * N * D).astype(np.float32) for _ in range(2))
+    k, v = (rng.uniform(-1, 1, batch * Hkv * N * D).astype(np.float32) for _ in range(2))
+    rp, ci = oracle.csr_all(cfg)
+    dq, dk, dv = oracle.attn_bwd(q, k, v, do, rp, ci, batch, H, Hkv, N, D, S)
+    q_rows = [(u, i) for u in range(batch * H) for i in (0, 1, S - 1, S, N // 2, N - 1)]
+    k_rows = [(g, j) for g in range(batch * Hkv) for j in (0, S - 1, S, 2 * S + 3, N - 1)]
+    sq, sk, sv = oracle.bwd_sample(q, k, v, do, rp, ci, batch, H, Hkv, N, D, S, q_rows, k_rows)
+    dq, dk, dv = dq.reshape(-1, N, D), dk.reshape(-1, N, D), dv.reshape(-1, N, D)
+    for n, (u, i) in enumerate(q_rows):
+        np.testing.assert_allclose(sq[n], dq[u, i], rtol=1e-5, atol=1e-6)
+    for n, (g, j) in enumerate(k_rows):
+        np.testing.assert_allclose(sk[n], dk[g, j], rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(sv[n], dv[g, j], rtol=1e-5, atol=1e-6)
