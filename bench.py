@@ -355,7 +355,9 @@ def run_s2(args):
         ho, hl, hdq, hdk, hdv = (torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
                                  for t in (out, lse, dq, dk, dv))
         e2e_steps = max(1, min(args.steps, 5))
-        e2e_api = "s2_attn_fwd_bwd_host (C ABI, host buffers, H2D/kernels/D2H pipelined over 16 unit chunks)"
+        chunks = int(os.environ.get("S2_E2E_CHUNKS", "32"))
+        e2e_api = (f"s2_attn_fwd_bwd_host (C ABI, host buffers, H2D/kernels/D2H pipelined over "
+                   f"{chunks} unit chunks)")
         if world == 1:
             # the host-resident data path of the public API: one call per step
             hq4, hk4, hv4, hdo4 = (t.reshape(1, U, N_SEQ, D) for t in (hq, hk, hv, hdo))
@@ -366,7 +368,7 @@ def run_s2(args):
 
             def e2e_step():
                 ws_holder[0] = s2.s2_attn_fwd_bwd_host(plan, hq4, hk4, hv4, hdo4, ho4, hl4, hdq4, hdk4, hdv4,
-                                                       num_chunks=16, workspace=ws_holder[0])
+                                                       num_chunks=chunks, workspace=ws_holder[0])
         else:
             e2e_api = "torch copies from pinned host memory + s2_attn_fwd/bwd on this rank's units"
 
@@ -394,7 +396,7 @@ def run_s2(args):
         d2h = sum(t.numel() * t.element_size() for t in (out, lse, dq, dk, dv))
         line["e2e"] = {"value": 3.5 * tot_fwd_flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
                        "ms_per_step": ems, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                       "api": e2e_api}
+                       "api": e2e_api, "pcie": pcie_bound(ho, hdq, out, dq, h2d, d2h, ems)}
 
     # ---- hybrid 24-layer mix of cfg3 (dense layers {0, 1}, configs/l1v15_dense01.json
     #      shape): one dense-causal layer through the same kernels (LayerStack),
@@ -427,6 +429,42 @@ def run_s2(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def pcie_bound(h_a, h_b, d_a, d_b, h2d, d2h, ems):
+    """The e2e path's floor on this box: pinned copies in both directions at once
+    (H2D into d_a while D2H out of d_b), measured here on scratch buffers of the
+    step's own tensors."""
+    import torch
+
+    s1, s2_ = torch.cuda.Stream(), torch.cuda.Stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def both():
+        ev = torch.cuda.Event()
+        ev.record()
+        s1.wait_event(ev)
+        s2_.wait_event(ev)
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_a, non_blocking=True)
+        with torch.cuda.stream(s2_):
+            h_b.copy_(d_b, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2_)
+
+    both()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(3):
+        both()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    nbytes = h_a.numel() * h_a.element_size() + h_b.numel() * h_b.element_size()
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    floor = (h2d + d2h) / (gbs * 1e9) * 1e3
+    return {"duplex_gbs": gbs, "floor_ms": floor, "frac_of_floor": floor / ems,
+            "note": "pinned H2D and D2H at once (the bytes of a step move no faster than this)"}
 
 
 def bench_decode(args, dev, world):
