@@ -16,11 +16,15 @@
 // softmax of this chunk runs, instead of after it.
 //
 // Warp roles (384 threads, 1 CTA / SM; setmaxnreg moves registers from the
-// control warpgroup (56/thread) to the two softmax warpgroups (224/thread)):
+// control warpgroup (72/thread) to the two softmax warpgroups (216/thread)):
 //   warp 0      TMA producer: Q tiles, one K/V chunk per NST ring stage
-//   warp 1      MMA issuer:  per chunk j: S_t(j) = Q_t K(j)^T for both tiles (SS,
-//               N=64), then O_t += P_t(j-1) V(j-1) (TS, K=64)
+//   warp 1      S issuer:   S_t(j) = Q_t K(j)^T for both tiles (SS, N=64), into
+//               S half j & 1 once the P V that last read that half is complete
 //   warp 2      TMEM allocator
+//   warp 3      P V issuer: O_t += P_t(j) V(j) (TS, K=64) as soon as P_t(j) is in
+//               TMEM; releases the K/V stage.  (tcgen05.mma issue blocks for about
+//               the MMA's execution time, so one warp that also waited for P left
+//               the pipe idle meanwhile: two issuers, 6-7% faster.)
 //   warps 4-7   softmax of tile 0 (thread = query row = TMEM lane), epilogue
 //   warps 8-11  softmax of tile 1
 // TMEM (512 columns): tile t owns [256t, 256t+256): S halves at +0 / +64 (P
@@ -105,11 +109,13 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar_qf[2], bar_qe[2], bar_kf[NST], bar_ke[NST];
-    // bar_pv[t]: completes once per P V of tile t (the softmax waits on it only to
-    // rescale O, which the previous chunk's P V may still be accumulating into).
-    // S / P barriers are per (tile, S half): the MMA warp runs one chunk ahead of
-    // the softmax, so a single barrier could complete two phases ahead of a waiter.
-    __shared__ uint64_t bar_sf[2][2], bar_pf[2][2], bar_of[2], bar_oe[2], bar_pv[2];
+    // bar_pv[t][h]: completes once per P V of tile t that read S half h (P V #m
+    // reads half m & 1).  The S issuer waits on it before overwriting that half
+    // (two MMA-issuing warps: no issue-order guarantee between them), the
+    // softmax before rescaling O.  S / P barriers are per (tile, S half) too:
+    // with two chunks in flight per tile, a single barrier could complete two
+    // phases ahead of a waiter.
+    __shared__ uint64_t bar_sf[2][2], bar_pf[2][2], bar_of[2], bar_oe[2], bar_pv[2][2];
     __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x;
@@ -128,7 +134,8 @@ __global__ void __launch_bounds__(384, 1)
             }
             mbar_init(smem_u32(&bar_of[i]), 1);
             mbar_init(smem_u32(&bar_oe[i]), 128);
-            mbar_init(smem_u32(&bar_pv[i]), 1);
+            mbar_init(smem_u32(&bar_pv[i][0]), 1);
+            mbar_init(smem_u32(&bar_pv[i][1]), 1);
         }
         for (int i = 0; i < NST; ++i) {
             mbar_init(smem_u32(&bar_kf[i]), 1);
@@ -146,7 +153,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tmem = tmem_base_s;
 
     if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;" ::: "memory");
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------------ producer
             tma_prefetch(&tmQ);
@@ -187,16 +194,17 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
         } else if (warp == 1) {
-            // ------------------------------------------------------ MMA issuer
-            // Whole warp on warp-uniform values, one elected lane issues (the
-            // descriptors stay in uniform registers: no per-MMA waterfall).
+            // ------------------------------------------------------ S issuer
+            // tcgen05.mma issue runs at about the rate the pipe executes it, so a
+            // warp that also waits for P leaves the pipe idle meanwhile.  S and
+            // P V therefore have their own issuing warps (1 and 3); the pipe is
+            // fed whenever either has work.  Whole warp on warp-uniform values,
+            // one elected lane issues (descriptors in uniform registers).
             constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);
-            constexpr uint32_t idO = umma_idesc_bf16(128, D, 0, 1);
             const bool leader = elect_one();
             const uint64_t dQ0 = umma_desc_sw128(sQ0, 16, 1024);
             const uint64_t dKV0 = umma_desc_sw128(sKV, 16, 1024);
-            const uint64_t dVmn0 = umma_desc_sw128(sKV + C::kCBytes, 8192, 1024);
-            uint32_t kv_it = 0, q_use[2] = {0, 0}, p_cnt[2] = {0, 0}, o_use[2] = {0, 0};
+            uint32_t kv_it = 0, q_use[2] = {0, 0};
             uint32_t k_cnt[2] = {0, 0};  // S of tile t issued so far (global): its S half
             const int i_end = p.sched[blockIdx.x + 1];
             for (int i = p.sched[blockIdx.x]; i < i_end; ++i) {
@@ -206,30 +214,6 @@ __global__ void __launch_bounds__(384, 1)
                 const bool has[2] = {true, has_b};
                 for (int t = 0; t < 2; ++t)
                     if (has[t]) mbar_wait(smem_u32(&bar_qf[t]), q_use[t] & 1);
-                int pend_st[2] = {-1, -1};   // stage of the chunk whose P V is pending
-                uint32_t pend_half[2] = {0, 0};
-                bool first_pv[2] = {true, true};
-                int prev_st = -1;             // stage of the previous chunk (released after its P Vs)
-                auto issue_pv = [&](int t) {
-                    const uint32_t tS = tmem + t * 256, tO = tS + 128;
-                    S2FTRACE(3 + 10 * t, p_cnt[t]);
-                    mbar_wait(smem_u32(&bar_pf[t][p_cnt[t] & 1]), (p_cnt[t] >> 1) & 1);
-                    S2FTRACE(12 + 2 * t, p_cnt[t]);
-                    ++p_cnt[t];
-                    if (first_pv[t] && o_use[t] > 0) mbar_wait(smem_u32(&bar_oe[t]), (o_use[t] - 1) & 1);
-                    tc_fence_after();  // P was written to TMEM by tcgen05.st
-                    const uint64_t dv = dVmn0 + static_cast<uint64_t>((pend_st[t] * C::kStageBytes) >> 4);
-                    if (leader) {
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            mma_ts(tO, tS + pend_half[t] * 64 + kk * 8, dv + ((kk * 2048) >> 4), idO,
-                                   (first_pv[t] && kk == 0) ? 0u : 1u);
-                        mma_commit(smem_u32(&bar_pv[t]));
-                    }
-                    __syncwarp();
-                    first_pv[t] = false;
-                    pend_st[t] = -1;
-                };
                 PairStep nxt = steps[0];
                 for (int n = 0; n < nsteps; ++n) {
                     const PairStep ps = nxt;
@@ -243,14 +227,14 @@ __global__ void __launch_bounds__(384, 1)
                         mbar_wait(smem_u32(&bar_kf[st]), (kv_it / NST) & 1);
                         S2FTRACE(1, kv_it);
                         const uint64_t dk = dKV0 + static_cast<uint64_t>((st * C::kStageBytes) >> 4);
-                        // S_t(j) for both tiles first: they run while P_t(j-1) is computed
-                        uint32_t s_half[2] = {0, 0};
 #pragma unroll
                         for (int t = 0; t < 2; ++t) {
                             if (!has[t] || !mk[t]) continue;
-                            s_half[t] = k_cnt[t] & 1;
-                            ++k_cnt[t];
-                            const uint32_t tS = tmem + t * 256 + s_half[t] * 64;
+                            const uint32_t kc = k_cnt[t]++;
+                            const uint32_t half = kc & 1;
+                            // the half holds P of S #kc-2: its P V must be complete
+                            if (kc >= 2) mbar_wait(smem_u32(&bar_pv[t][half]), ((kc - 2) >> 1) & 1);
+                            const uint32_t tS = tmem + t * 256 + half * 64;
                             const uint64_t dq = dQ0 + static_cast<uint64_t>((t * C::kQBytes) >> 4);
                             if (leader) {
 #pragma unroll
@@ -259,36 +243,11 @@ __global__ void __launch_bounds__(384, 1)
                                     const uint32_t ok = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
                                     mma_ss(tS, dq + oq, dk + ok, idS, kk > 0);
                                 }
-                                mma_commit(smem_u32(&bar_sf[t][s_half[t]]));
+                                mma_commit(smem_u32(&bar_sf[t][half]));
                             }
                             __syncwarp();
                         }
                         S2FTRACE(2, kv_it);
-                        // then the pending P V of each tile (chunk j-1 or earlier)
-#pragma unroll
-                        for (int t = 0; t < 2; ++t)
-                            if (pend_st[t] >= 0 && (has[t] && mk[t])) issue_pv(t);
-                        // chunk j-1's stage is free once every P V reading it is issued
-                        if (prev_st >= 0 && pend_st[0] != prev_st && pend_st[1] != prev_st) {
-                            if (leader) mma_commit(smem_u32(&bar_ke[prev_st]));
-                            __syncwarp();
-                            prev_st = -1;
-                        }
-#pragma unroll
-                        for (int t = 0; t < 2; ++t)
-                            if (has[t] && mk[t]) {
-                                pend_st[t] = st;
-                                pend_half[t] = s_half[t];
-                            }
-                        if (prev_st >= 0) {  // a tile skipped chunk j: its older P V holds prev_st
-                            // (flush: issue the held P V now so the stage can be released)
-#pragma unroll
-                            for (int t = 0; t < 2; ++t)
-                                if (pend_st[t] == prev_st) issue_pv(t);
-                            if (leader) mma_commit(smem_u32(&bar_ke[prev_st]));
-                            __syncwarp();
-                        }
-                        prev_st = st;
                         ++kv_it;
                     }
                 }
@@ -298,28 +257,87 @@ __global__ void __launch_bounds__(384, 1)
                     for (int t = 0; t < 2; ++t)
                         if (has[t]) mma_commit(smem_u32(&bar_qe[t]));
                 __syncwarp();
-                // each tile's O is final after its own last P V (no wait on the other tile)
-#pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    if (pend_st[t] >= 0) issue_pv(t);
-                    if (has[t]) {
-                        if (leader) mma_commit(smem_u32(&bar_of[t]));
-                        __syncwarp();
+                for (int t = 0; t < 2; ++t)
+                    if (has[t]) ++q_use[t];
+            }
+        } else if (warp == 3) {
+            // ------------------------------------------------------ P V issuer
+            constexpr uint32_t idO = umma_idesc_bf16(128, D, 0, 1);
+            const bool leader = elect_one();
+            const uint64_t dVmn0 = umma_desc_sw128(sKV + C::kCBytes, 8192, 1024);
+            uint32_t kv_it = 0, p_cnt[2] = {0, 0}, o_use[2] = {0, 0};
+            const int i_end = p.sched[blockIdx.x + 1];
+            for (int i = p.sched[blockIdx.x]; i < i_end; ++i) {
+                const int nsteps = warp_uniform(p.items[i].nsteps);
+                const bool has_b = warp_uniform(p.items[i].has_b) != 0;
+                const PairStep* steps = p.steps + p.items[i].step_off;
+                const bool has[2] = {true, has_b};
+                bool first_pv[2] = {true, true};
+                int last_chunk[2] = {-1, -1};  // this item's last attended chunk per tile
+                for (int n = 0; n < nsteps; ++n) {
+                    const PairStep ps = steps[n];
+                    for (int h = 0; h < 2; ++h) {
+                        const int chunk = h ? ps.c1 : ps.c0;
+                        if (chunk < 0) continue;
+                        const int kc = n * 2 + h;
+                        if (has[0] && (h ? ps.a1 : ps.a0)) last_chunk[0] = kc;
+                        if (has[1] && (h ? ps.b1 : ps.b0)) last_chunk[1] = kc;
                     }
                 }
-                if (prev_st >= 0) {
-                    if (leader) mma_commit(smem_u32(&bar_ke[prev_st]));
-                    __syncwarp();
+                last_chunk[0] = warp_uniform(last_chunk[0]);
+                last_chunk[1] = warp_uniform(last_chunk[1]);
+                PairStep nxt = steps[0];
+                for (int n = 0; n < nsteps; ++n) {
+                    const PairStep ps = nxt;
+                    if (n + 1 < nsteps) nxt = steps[n + 1];
+                    for (int h = 0; h < 2; ++h) {
+                        const int chunk = warp_uniform(h ? ps.c1 : ps.c0);
+                        if (chunk < 0) continue;
+                        const uint32_t mk[2] = {warp_uniform(h ? ps.a1 : ps.a0), warp_uniform(h ? ps.b1 : ps.b0)};
+                        const int st = kv_it % NST;
+                        const uint64_t dv = dVmn0 + static_cast<uint64_t>((st * C::kStageBytes) >> 4);
+#pragma unroll
+                        for (int t = 0; t < 2; ++t) {
+                            if (!has[t] || !mk[t]) continue;
+                            const uint32_t m = p_cnt[t]++;
+                            const uint32_t half = m & 1;
+                            const uint32_t tS = tmem + t * 256 + half * 64, tO = tmem + t * 256 + 128;
+                            S2FTRACE(3 + 10 * t, m);
+                            mbar_wait(smem_u32(&bar_pf[t][half]), (m >> 1) & 1);
+                            S2FTRACE(12 + 2 * t, m);
+                            if (first_pv[t] && o_use[t] > 0) mbar_wait(smem_u32(&bar_oe[t]), (o_use[t] - 1) & 1);
+                            tc_fence_after();  // P was written to TMEM by tcgen05.st
+                            if (leader) {
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk)
+                                    mma_ts(tO, tS + kk * 8, dv + ((kk * 2048) >> 4), idO,
+                                           (first_pv[t] && kk == 0) ? 0u : 1u);
+                                mma_commit(smem_u32(&bar_pv[t][half]));
+                                // O of tile t is final after its last P V of the item
+                                if (n * 2 + h == last_chunk[t]) mma_commit(smem_u32(&bar_of[t]));
+                            }
+                            __syncwarp();
+                            first_pv[t] = false;
+                        }
+                        // stage st: K was read by the S MMAs (complete: their P existed),
+                        // V by the P V just issued
+                        if (leader) mma_commit(smem_u32(&bar_ke[st]));
+                        __syncwarp();
+                        ++kv_it;
+                    }
                 }
                 for (int t = 0; t < 2; ++t)
                     if (has[t]) {
+                        if (last_chunk[t] < 0) {  // (a tile with no attended chunk: O is never written)
+                            if (leader) mma_commit(smem_u32(&bar_of[t]));
+                            __syncwarp();
+                        }
                         ++o_use[t];
-                        ++q_use[t];
                     }
             }
         }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 216;" ::: "memory");
         // ------------------------------------------------------- softmax WGs
         const int t = (warp >> 2) - 1;         // tile 0: warps 4-7, tile 1: warps 8-11
         const int r = tid & 127;               // row in tile == TMEM lane
@@ -382,7 +400,8 @@ __global__ void __launch_bounds__(384, 1)
                         // O must hold every earlier chunk's P V before it is rescaled: the
                         // last one issued is this tile's chunk k_here-1 (its (k_here-1)-th
                         // P V overall), still possibly in flight
-                        if (k_here > 0) mbar_wait(smem_u32(&bar_pv[t]), (k_here - 1) & 1);
+                        if (k_here > 0)
+                            mbar_wait(smem_u32(&bar_pv[t][(k_here - 1) & 1]), ((k_here - 1) >> 1) & 1);
                         tc_fence_after();
                         const float alpha = rescale ? fast_exp2(m_run - m_use) : 1.0f;
                         l_run *= alpha;
