@@ -193,3 +193,32 @@ def test_cfg2_batch4_fwd_bwd_rows_match_oracle():
     for n, (u, j) in enumerate(k_rows):
         np.testing.assert_allclose(gk[u, j], rk[n], **TOL, err_msg=f"dk unit {u} key {j}")
         np.testing.assert_allclose(gv[u, j], rv[n], **TOL, err_msg=f"dv unit {u} key {j}")
+
+
+def test_512k_forward_backward_rows_match_oracle():
+    """Past the largest BASELINE config (128K): a 512K-token layer (B=8192 blocks,
+    32 heads) -- the plan's lists, the persistent schedules and 64-bit offsets at
+    4 GB per tensor.  Sampled forward rows and the dK/dV identities."""
+    torch = _torch()
+    cfg = s2.make_s2_config(524288, 32, block_size=64, local_blocks=4, vert_stride=16)
+    N, H, D, S = cfg.seq_len, cfg.num_heads, 128, cfg.block_size
+    g = torch.Generator(device="cuda").manual_seed(36)
+    q, k, v, do = (_uniform((1, H, N, D), g) for _ in range(4))
+    plan = s2.Plan.from_config(cfg)
+    out, lse = s2.s2_attn_fwd(plan, q, k, v)
+    dq, dk, dv = s2.s2_attn_bwd(plan, q, k, v, out, lse, do)
+    torch.cuda.synchronize()
+    heads = [1, 31]
+    rp, ci = oracle.csr_all(cfg)
+    srp, sci = _csr_heads(rp, ci, cfg.num_blocks(), heads)
+    hk = np.ascontiguousarray(_host(k[:, heads]).ravel())
+    hv = np.ascontiguousarray(_host(v[:, heads]).ravel())
+    for t in (0, 300001, N - 1):
+        ro, rl = oracle.decode(_host(q[:, heads, t]).ravel(), hk, hv, srp, sci, 1, 2, 2, N, D, S, t,
+                               cfg.num_blocks())
+        np.testing.assert_allclose(_host(out[:, heads, t]).ravel(), ro, **TOL, err_msg=f"out row {t}")
+        np.testing.assert_allclose(lse[:, heads, t].cpu().numpy().ravel(), rl, **TOL)
+    for h in heads:  # sum_j dV_j = sum_i dO_i ; sum_j dK_j = 0
+        sdv, sdo = dv[0, h].double().sum(0), do[0, h].double().sum(0)
+        assert torch.all((sdv - sdo).abs() <= 1e-3 * dv[0, h].double().abs().sum(0) + 1e-3)
+        assert torch.all(dk[0, h].double().sum(0).abs() <= 1e-3 * dk[0, h].double().abs().sum(0) + 1e-3)
