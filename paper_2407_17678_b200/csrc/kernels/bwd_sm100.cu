@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
+    if (p.trace && tid == 0) p.trace[15 * 2048 + 2 * blockIdx.x] = globaltimer_ns();  // debug: CTA start
     // TMEM: V at 0 (the dP^T A operand: copied in once per item with tcgen05.cp, so
     // the per-step dP^T MMAs read only the 2 KB dO slices from shared memory),
     // S^T[b] at 64+64b (the elementwise warps write P^T and dS^T back into it: warp
@@ -518,6 +519,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (p.trace && tid == 0) p.trace[15 * 2048 + 2 * blockIdx.x + 1] = globaltimer_ns();  // debug: CTA end
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -581,6 +583,7 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
+    if (p.trace && tid == 0) p.trace[15 * 2048 + 2 * blockIdx.x] = globaltimer_ns();  // debug: CTA start
     // TMEM: Q at 0 and dO at 64 (the S / dP A operands, copied in with tcgen05.cp once
     // per item: the per-step MMAs then read only the 2 KB K / V slices from shared
     // memory), S[b] at 128+64b, dP[b] at 256+64b, dQ at 384.
@@ -788,6 +791,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (p.trace && tid == 0) p.trace[15 * 2048 + 2 * blockIdx.x + 1] = globaltimer_ns();  // debug: CTA end
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);

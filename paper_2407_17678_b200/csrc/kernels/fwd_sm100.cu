@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
+    if (p.trace && tid == 0) p.trace[15 * 2048 + 2 * blockIdx.x] = globaltimer_ns();  // debug: CTA start
 
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 72;" ::: "memory");
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (p.trace && tid == 0) p.trace[15 * 2048 + 2 * blockIdx.x + 1] = globaltimer_ns();  // debug: CTA end
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
