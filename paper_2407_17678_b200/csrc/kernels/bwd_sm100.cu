@@ -140,10 +140,12 @@ __global__ void __launch_bounds__(384, 1)
     // bar_kvf[kb]: K buffer kb and the V buffer hold the item's tiles.
     // bar_kve[kb]: K buffer kb is free (its item's last S^T MMA done AND the
     // epilogue TMA stores staged in it have read it): count 2.
-    // bar_ve: the item's V has been copied into TMEM (the V buffer is free).
+    // bar_vcp: the item's V has been copied into TMEM.  bar_ve (count 2): the V
+    // buffer may be refilled -- the copy is done AND the previous item's
+    // epilogue, which stages dK in the V buffer, has been stored.
     // bar_dpf: the elementwise warps have read dP^T (its single TMEM buffer is free).
     struct Bars {
-        uint64_t kvf[2], kve[2], ve, sf[NST], se[NST], s[2], p[2], af, ae, dpf;
+        uint64_t kvf[2], kve[2], ve, vcp, sf[NST], se[NST], s[2], p[2], af, ae, dpf;
         uint32_t tmem_base;
     };
     static_assert(sizeof(Bars) <= C::kDkvBars, "barrier block");
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(384, 1)
     auto& bar_kvf = bars.kvf;
     auto& bar_kve = bars.kve;
     auto& bar_ve = bars.ve;
+    auto& bar_vcp = bars.vcp;
     auto& bar_sf = bars.sf;
     auto& bar_se = bars.se;
     auto& bar_s = bars.s;
@@ -172,7 +175,8 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(smem_u32(&bar_kvf[i]), 1);
             mbar_init(smem_u32(&bar_kve[i]), 2);
         }
-        mbar_init(smem_u32(&bar_ve), 1);
+        mbar_init(smem_u32(&bar_ve), 2);
+        mbar_init(smem_u32(&bar_vcp), 1);
         mbar_init(smem_u32(&bar_af), 1);
         mbar_init(smem_u32(&bar_ae), 256);
         for (int i = 0; i < NST; ++i) {
@@ -287,7 +291,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk)
                         tmem_cp_128x256b(tmem + kk * 8, dV0 + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4));
-                    mma_commit(smem_u32(&bar_ve));  // the V buffer may be refilled
+                    mma_commit(smem_u32(&bar_vcp));  // V is in TMEM
+                    mma_commit(smem_u32(&bar_ve));   // (+ the previous epilogue's dK store)
                 }
                 __syncwarp();
                 auto accumulate = [&](uint32_t n, int st, bool first) {
@@ -367,7 +372,8 @@ __global__ void __launch_bounds__(384, 1)
         const int cg = (kr & 63) >> 4;
         const int hk = kr >> 6;
         uint32_t it_cnt = 0, st_it = 0;
-        int release = -1;  // WG leader: K/V buffer whose epilogue store is still in flight
+        int release = -1;  // WG leader: K buffer (and the V buffer) whose epilogue stores are in flight
+        if (tid == 128) mbar_arrive(smem_u32(&bar_ve));  // no epilogue before the first item
         for (int i = i_beg; i < i_end; ++i, ++it_cnt) {
             const BwdItem it = items[i];
             const int chunk = hk ? it.c1 : it.c0;
@@ -445,9 +451,10 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_before();
                 mbar_arrive(smem_u32(&bar_p[b]));
                 if (tid == 128) S2TRACE(7, st_it);
-                if (release >= 0) {  // the previous item's store read its staging long ago
+                if (release >= 0) {  // the previous item's stores read their staging long ago
                     bulk_wait_read0();
                     mbar_arrive(smem_u32(&bar_kve[release]));
+                    mbar_arrive(smem_u32(&bar_ve));
                     release = -1;
                 }
             }
@@ -475,19 +482,20 @@ __global__ void __launch_bounds__(384, 1)
             if (release >= 0) {  // (an item without steps: release here at the latest)
                 bulk_wait_read0();
                 mbar_arrive(smem_u32(&bar_kve[release]));
+                mbar_arrive(smem_u32(&bar_ve));
                 release = -1;
             }
-            // bar_af: every MMA of the item is done, so its K tile is dead
-            const uint32_t sOut = sK + (it_cnt & 1) * C::kTile128;
-            const uint32_t so = sOut + hk * (C::kSub * 8192) + (kr & 63) * 128;
+            const bool has_next = i + 1 < i_end;
+            // bar_af: every MMA of the item is done, so its K tile is dead: dV is
+            // staged there.  dK goes to the V buffer once the next item's V has been
+            // copied into TMEM (the producer refills it only after these stores).
 #pragma unroll
             for (int ph = 0; ph < 2; ++ph) {  // 0: dV, 1: dK (scaled)
                 const uint32_t* acc = ph ? ak : av;
                 const float mul = ph ? p.scale : 1.0f;
-                if (ph == 1) {  // the dV stores must have read the staging tile
-                    if (st_leader) bulk_wait_read0();
-                    named_bar_sync(1, 256);
-                }
+                const uint32_t sOut = ph ? sV : sK + (it_cnt & 1) * C::kTile128;
+                const uint32_t so = sOut + hk * (C::kSub * 8192) + (kr & 63) * 128;
+                if (ph == 1 && has_next) mbar_wait(smem_u32(&bar_vcp), (it_cnt + 1) & 1);
 #pragma unroll
                 for (int j = 0; j < D / 16; ++j) {
                     const int c = wg * (D / 16) + j;  // 16-byte chunk of the row: D/64 slice c>>3
@@ -511,7 +519,7 @@ __global__ void __launch_bounds__(384, 1)
                     bulk_commit();
                 }
             }
-            if (st_leader) release = static_cast<int>(it_cnt & 1);  // arrive on bar_kve once the stores have read it
+            if (st_leader) release = static_cast<int>(it_cnt & 1);  // arrive on bar_kve / bar_ve once read
             if (tid == 128) S2TRACE(10, it_cnt);
         }
         if (tid == 128) bulk_wait0();  // staging tiles must outlive the stores
