@@ -243,14 +243,23 @@ def run_s2(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test-only switches (tests/test_gpu_multirank.py): S2_BENCH_SHARE_GPU=1 puts
+    # every rank on cuda:0 and S2_BENCH_BACKEND=gloo replaces NCCL, so the
+    # multi-rank path runs on a one-GPU box.  Never a performance configuration.
+    if os.environ.get("S2_BENCH_SHARE_GPU") == "1":
+        local = 0
+    backend = os.environ.get("S2_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        # NCCL's all-gather CTAs share the GPU with the backward: cap them and
-        # keep their SMs out of the persistent kernels' grid (s2_set_sm_reserve)
-        os.environ.setdefault("NCCL_MAX_CTAS", str(COMM_SMS))
-        dist.init_process_group("nccl", device_id=dev)
-        _abi.check(_abi.lib().s2_set_sm_reserve(int(os.environ["NCCL_MAX_CTAS"])))
+        if backend == "nccl":
+            # NCCL's all-gather CTAs share the GPU with the backward: cap them and
+            # keep their SMs out of the persistent kernels' grid (s2_set_sm_reserve)
+            os.environ.setdefault("NCCL_MAX_CTAS", str(COMM_SMS))
+            dist.init_process_group("nccl", device_id=dev)
+            _abi.check(_abi.lib().s2_set_sm_reserve(int(os.environ["NCCL_MAX_CTAS"])))
+        else:
+            dist.init_process_group(backend)
     cfg = workload_cfg()
     plan = s2.Plan.from_config(cfg)
     hp = HeadParallelPlan(plan, world, world)  # global batch = world (weak scaling)

@@ -1,0 +1,101 @@
+"""Multi-rank path with the real kernels on a one-GPU box.
+
+Two processes share cuda:0 and talk over gloo (NCCL refuses two ranks on one
+device; the driver's 8-GPU runs use NCCL). This covers with the sm_100a kernels
+what tests/test_dist_gloo.py covers with the oracle:
+  * head_parallel_forward's gathered O / lse are bit-identical to one process
+    (head-permutation exactness, test_attention.cpp:217-240), and each rank's
+    backward on its own units equals the single-process gradients of those units;
+  * bench.py launched by torchrun at world size 2 prints one valid JSON line
+    (n_gpus 2, weak scaling, positive throughput) -- a code-path check, not a
+    performance number (both ranks time-slice one GPU).
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from helpers import single
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cfg, batch, D, res_path):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_17678_b200 as s2
+    from paper_2407_17678_b200.dist import HeadParallelPlan, head_parallel_forward
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plan = s2.Plan.from_config(cfg)
+    N, H, Hkv = cfg.seq_len, cfg.num_heads, cfg.kv_heads()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    mk = lambda h: (torch.rand((batch, h, N, D), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)  # noqa
+    q, k, v, do = mk(H), mk(Hkv), mk(Hkv), mk(H)
+    hp = HeadParallelPlan(plan, batch, world)
+    out, lse = head_parallel_forward(plan, q, k, v, rank, world, hp=hp)
+    # this rank's backward on its own units (the gradients stay sharded)
+    units = hp.units[rank]
+    grads = None
+    if len(units):
+        ql, kl, vl, dol = hp.scatter_q(q, rank), hp.scatter_kv(k, rank), hp.scatter_kv(v, rank), hp.scatter_q(do, rank)
+        ol, ll = s2.s2_attn_fwd(plan, ql, kl, vl, unit_ids=units)
+        grads = s2.s2_attn_bwd(plan, ql, kl, vl, ol, ll, dol, unit_ids=units)
+    torch.cuda.synchronize()
+    if rank == 0:
+        ref_out, ref_lse = s2.s2_attn_fwd(plan, q, k, v)
+        rq, rk, rv = s2.s2_attn_bwd(plan, q, k, v, ref_out, ref_lse, do)
+        ok = torch.equal(out, ref_out) and torch.equal(lse, ref_lse)
+        if grads is not None:
+            qu = torch.as_tensor(units, device="cuda")
+            ok = ok and torch.equal(grads[0], rq.reshape(batch * Hkv, -1, N, D)[qu])
+            ok = ok and torch.equal(grads[1], rk.reshape(batch * Hkv, N, D)[qu])
+            ok = ok and torch.equal(grads[2], rv.reshape(batch * Hkv, N, D)[qu])
+        with open(res_path, "w") as f:
+            f.write("ok" if ok else "MISMATCH")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["mha_b2", "gqa"])
+def test_head_parallel_world2_on_one_gpu_is_bit_identical(case, tmp_path):
+    import torch.multiprocessing as mp
+
+    if case == "mha_b2":
+        cfg, batch, D = single(1024, 64, 4, 2, 4), 2, 128
+    else:
+        cfg, batch, D = single(2048, 64, 8, 4, 4, kv=2), 1, 128
+    res = str(tmp_path / "res.txt")
+    mp.spawn(_worker, args=(2, _free_port(), cfg, batch, D, res), nprocs=2, join=True)
+    assert open(res).read() == "ok"
+
+
+def test_bench_world2_prints_one_valid_line():
+    env = dict(os.environ, S2_BENCH_SHARE_GPU="1", S2_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu-baseline", "--no-decode",
+           "--no-hybrid"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-3000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["steps"] == 3
+    assert d["config"]["global_batch"] == 2
