@@ -159,11 +159,13 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def config_desc(n):
+def config_desc(n, exchange="allgather"):
+    how = ("forward stores O into every rank's output (fused exchange)" if exchange == "fused" and n > 1
+           else "all-gather of O")
     return {"workload": "cfg3: one S2 attention layer fwd+bwd, S=32768, H=32, D=128, block 64, "
                         "local_blocks 4, vert_stride 16, heterogeneous head offsets",
             "batch_per_gpu": 1, "global_batch": n, "seq_len": N_SEQ, "heads": H, "head_dim": D,
-            "parallelism": f"head-parallel x{n} (LPT by active blocks), all-gather of O",
+            "parallelism": f"head-parallel x{n} (LPT by active blocks), {how}",
             "l2": "inputs 256 MiB per tensor > 126 MB L2; no flush needed"}
 
 
@@ -280,7 +282,25 @@ def run_s2(args):
     tot_fwd_flops = float(w.sum()) * per_pair
     dense_fwd_total = dense1 * world
 
+    fused = world > 1 and args.exchange == "fused"
+    if fused:
+        # the forward stores every O tile straight into each rank's full output
+        # (peer memory); one tiny collective per step orders the ranks' kernels
+        from paper_2407_17678_b200.dist import PeerOutputs
+
+        peers = PeerOutputs(hp, N_SEQ, D, torch.bfloat16, dev, rank)
+        unit_global = torch.as_tensor(np.asarray(units, dtype=np.int32), device=dev)
+        fence = torch.zeros(1, device=dev)
+
     def step():
+        if fused:
+            s2.s2_attn_fwd_peers(plan, q, k, v, unit_ids=units, peer_out=peers.peer_out, peer_lse=peers.peer_lse,
+                                 unit_global=unit_global, total_units=peers.total_units, out=out, lse=lse)
+            # the backward needs only this rank's units; the fence after it makes
+            # every rank's forward (and so every peer write) complete
+            s2.s2_attn_bwd(plan, q, k, v, out, lse, do, dq=dq, dk=dk, dv=dv, unit_ids=units)
+            dist.all_reduce(fence)
+            return
         s2.s2_attn_fwd(plan, q, k, v, out=out, lse=lse, unit_ids=units)
         finish = hp.all_gather_async(out.reshape(U, 1, N_SEQ, D)) if world > 1 else None
         # the backward needs only this rank's units: it overlaps the all-gather
@@ -348,7 +368,7 @@ def run_s2(args):
         "metric": "S2 attn fwd+bwd active-block TFLOP/s @32K", "value": value, "unit": "TFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (U[-1,1] bf16)", "config": config_desc(world),
+        "data": "synthetic (U[-1,1] bf16)", "config": config_desc(world, args.exchange),
         "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
         "dense_equiv_tflops": 3.5 * dense_fwd_total / (ms_max * 1e-3) / 1e12,
         "dense_causal_fwd_bwd_flops_per_gpu": 3.5 * dense1,
@@ -606,6 +626,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-hybrid", action="store_true")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "fused"],
+                    help="N>1: NCCL all-gather of O overlapped with the backward (default), or the "
+                         "forward storing O straight into every rank's output (s2_attn_fwd_peers)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

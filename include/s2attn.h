@@ -186,6 +186,23 @@ typedef struct s2_attn_args {
 } s2_attn_args;
 int s2_attn_fwd(s2_plan* plan, const s2_attn_args* args, s2_stream_t stream);
 
+/* Forward with the head-parallel output exchange fused in (no reference
+ * symbol): besides args->out / args->lse (this rank's packed
+ * units), every finished O tile is TMA-stored into each of the num_peers
+ * ranks' FULL output buffers, and its lse rows written there.  The forward and
+ * the all-gather become one kernel; peer memory is reached over NVLink P2P
+ * (buffers mapped with CUDA IPC or symmetric memory).
+ *   peer_out[r]  bf16 [total_units, H/Hkv, N, D] of rank r (device pointer valid here)
+ *   peer_lse[r]  fp32 [total_units, H/Hkv, N]
+ *   unit_global  device int[num_units]: global unit index of each local unit
+ *                (the full layouts are unit-major, as with unit_ids == NULL)
+ * Requires the bf16 tcgen05 path and args->unit_ids; 1 <= num_peers <= 8.
+ * The caller orders the ranks' completion (e.g. a barrier after the kernel)
+ * before reading the full buffers. */
+int s2_attn_fwd_peers(s2_plan* plan, const s2_attn_args* args, int num_peers, void* const* peer_out,
+                      float* const* peer_lse, const int* unit_global, int total_units,
+                      s2_stream_t stream);
+
 /* ---- backward (no reference symbol: SPEC.md:262) ------------------------ */
 /* dQ kernel walks the CSR tile list, dK/dV kernel walks the transposed (CSC)
  * tile list; every dK/dV tile is owned by exactly one CTA (no atomics). */

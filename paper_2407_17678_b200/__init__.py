@@ -9,7 +9,7 @@ from .pattern import (  # noqa: F401
     make_multi_stride_config, make_s2_config, make_single_stride_config,
     make_sliding_window_config, nnz, same_bits, to_csr)
 from .attention import (  # noqa: F401
-    AttentionTensors, Plan, dsplit_attention, s2_attention, s2_attn_bwd, s2_attn_fwd, s2_attn_fwd_bwd_host,
+    AttentionTensors, Plan, dsplit_attention, s2_attention, s2_attn_bwd, s2_attn_fwd, s2_attn_fwd_bwd_host, s2_attn_fwd_peers,
     streaming_sharded_attention)
 from .serialize import (  # noqa: F401
     CliConfigFile, config_hash, csr_from_json, layer_schedule_from_json, load_config_file,

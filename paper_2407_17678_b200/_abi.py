@@ -115,6 +115,8 @@ SIGNATURES = {
                                ctypes.POINTER(ctypes.c_uint32)]),
     "s2_plan_bwd_tiles": (_I, [_P, _I64P, _I64P, _I64P, _I64P]),
     "s2_attn_fwd": (_I, [_P, ctypes.POINTER(s2_attn_args), _P]),
+    "s2_attn_fwd_peers": (_I, [_P, ctypes.POINTER(s2_attn_args), _I, ctypes.POINTER(ctypes.c_void_p),
+                               ctypes.POINTER(ctypes.c_void_p), _P, _I, _P]),
     "s2_attn_bwd_workspace_size": (_I, [_P, ctypes.POINTER(s2_attn_bwd_args),
                                         ctypes.POINTER(ctypes.c_size_t)]),
     "s2_attn_bwd": (_I, [_P, ctypes.POINTER(s2_attn_bwd_args), _P, ctypes.c_size_t, _P]),

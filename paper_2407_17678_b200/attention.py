@@ -181,6 +181,34 @@ def s2_attn_fwd(plan: Plan, q, k, v, *, scale: Optional[float] = None, num_split
     return out, lse
 
 
+def s2_attn_fwd_peers(plan: Plan, q, k, v, *, unit_ids, peer_out, peer_lse, unit_global, total_units: int,
+                      scale: Optional[float] = None, out=None, lse=None, stream=None):
+    """Forward of this rank's packed units with the output exchange fused in
+    (s2_attn_fwd_peers): every O tile also lands in each rank's full output
+    (`peer_out[r]` [total_units, hpg, N, D], `peer_lse[r]` [total_units, hpg, N],
+    device tensors mapped into this process), at the global unit
+    `unit_global[i]` (int32 device tensor) of local unit i.  Returns the local
+    (out, lse); the caller orders the ranks' completion before reading the
+    full buffers."""
+    import torch
+
+    _require_cuda(q, k, v, unit_global, *peer_out, *peer_lse)
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty(q.shape[:-1], device=q.device, dtype=torch.float32)
+    a, keep = _fwd_args(plan, q, k, v, out, lse, scale, 1, unit_ids)
+    n = len(peer_out)
+    if len(peer_lse) != n:
+        raise _abi.S2InvalidArgument(1, "peer_out and peer_lse differ in length")
+    po = (ctypes.c_void_p * n)(*[t.data_ptr() for t in peer_out])
+    pl = (ctypes.c_void_p * n)(*[t.data_ptr() for t in peer_lse])
+    ug = unit_global.to(torch.int32).contiguous()
+    check(lib().s2_attn_fwd_peers(plan.handle, ctypes.byref(a), n, po, pl, ctypes.c_void_p(ug.data_ptr()),
+                                  int(total_units), _stream_ptr(stream)))
+    return out, lse
+
+
 def s2_attn_bwd(plan: Plan, q, k, v, out, lse, dout, *, scale: Optional[float] = None,
                 dq=None, dk=None, dv=None, unit_ids=None, stream=None):
     """Sparse backward: (dq, dk, dv).  dK/dV tiles are owned by one CTA each (no atomics)."""

@@ -17,7 +17,9 @@
 cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtensorMap& k,
                                 const CUtensorMap& v, const CUtensorMap& o, const void* items, const int* sched,
                                 int grid, const void* steps, __nv_bfloat16* out, float* lse,
-                                int seq_len, int hpg, float scale_log2, cudaStream_t stream);
+                                int seq_len, int hpg, float scale_log2, cudaStream_t stream,
+                                int num_peers, const int* unit_global, float* const* peer_lse,
+                                const CUtensorMap* peer_o);
 cudaError_t s2_launch_fwd_simt(bool bf16, const void* q, const void* k, const void* v, void* out,
                                float* lse, const int* bh_list, const int* head_of, int num_bh,
                                const int* row_ptr, const int* col_idx, const int64_t* col_off,
@@ -655,7 +657,9 @@ int s2_partition_lpt(int num_units, const int64_t* weights, int num_ranks, int* 
     return S2_OK;
 }
 
-int s2_attn_fwd(s2_plan* p, const s2_attn_args* a, s2_stream_t stream) {
+static int attn_fwd_impl(s2_plan* p, const s2_attn_args* a, int num_peers, void* const* peer_out,
+                         float* const* peer_lse, const int* unit_global, int total_units,
+                         s2_stream_t stream) {
     if (int rc = check_args(p, a)) return rc;
     std::lock_guard<std::mutex> lk(p->mu);
     const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -668,6 +672,8 @@ int s2_attn_fwd(s2_plan* p, const s2_attn_args* a, s2_stream_t stream) {
     if (!w) return rc;
     const int nu = a->unit_ids ? a->num_units : a->batch * p->num_kv_heads;
     cudaError_t e;
+    if (num_peers > 0 && !use_tcgen05(p, a))
+        return fail(S2_ERR_UNSUPPORTED, "the fused output exchange needs the bf16 tcgen05 path");
     if (use_tcgen05(p, a)) {
         try {
             const uint64_t N = a->seq_len, D = a->head_dim;
@@ -675,10 +681,14 @@ int s2_attn_fwd(s2_plan* p, const s2_attn_args* a, s2_stream_t stream) {
             const CUtensorMap mk = s2host::make_map_bf16_3d(a->k, D, N, nu, 64, 64);
             const CUtensorMap mv = s2host::make_map_bf16_3d(a->v, D, N, nu, 64, 64);
             const CUtensorMap mo = s2host::make_map_bf16_3d(a->out, D, N, uint64_t(nu) * hpg, 64, 128);
+            CUtensorMap peer_maps[8];
+            for (int r = 0; r < num_peers; ++r)
+                peer_maps[r] = s2host::make_map_bf16_3d(peer_out[r], D, N, uint64_t(total_units) * hpg, 64, 128);
             ProfScope prof("fwd_sm100", st);
             e = s2_launch_fwd_sm100(a->head_dim, mq, mk, mv, mo, w->pair.ptr, w->pair_sched.as<int>(),
                                     w->grid, L->d_steps.ptr, static_cast<__nv_bfloat16*>(a->out),
-                                    a->lse, a->seq_len, hpg, float(scale * M_LOG2E), st);
+                                    a->lse, a->seq_len, hpg, float(scale * M_LOG2E), st, num_peers,
+                                    unit_global, peer_lse, peer_maps);
         } catch (const std::exception& ex) {
             return fail(S2_ERR_CUDA, ex.what());
         }
@@ -695,6 +705,26 @@ int s2_attn_fwd(s2_plan* p, const s2_attn_args* a, s2_stream_t stream) {
     }
     if (e != cudaSuccess) return cuda_fail(e, "s2_attn_fwd launch");
     return S2_OK;
+}
+
+int s2_attn_fwd(s2_plan* p, const s2_attn_args* a, s2_stream_t stream) {
+    return attn_fwd_impl(p, a, 0, nullptr, nullptr, nullptr, 0, stream);
+}
+
+int s2_attn_fwd_peers(s2_plan* p, const s2_attn_args* a, int num_peers, void* const* peer_out,
+                      float* const* peer_lse, const int* unit_global, int total_units,
+                      s2_stream_t stream) {
+    if (num_peers < 1 || num_peers > 8)
+        return fail(S2_ERR_INVALID_ARGUMENT, "num_peers must be in [1, 8]");
+    if (!peer_out || !peer_lse || !unit_global || !a || !a->unit_ids)
+        return fail(S2_ERR_INVALID_ARGUMENT,
+                    "peer_out, peer_lse, unit_global and the local unit_ids are required");
+    if (total_units < a->num_units)
+        return fail(S2_ERR_INVALID_ARGUMENT, "total_units is smaller than the local unit count");
+    for (int r = 0; r < num_peers; ++r)
+        if (!peer_out[r] || !peer_lse[r])
+            return fail(S2_ERR_INVALID_ARGUMENT, "null peer buffer");
+    return attn_fwd_impl(p, a, num_peers, peer_out, peer_lse, unit_global, total_units, stream);
 }
 
 }  // extern "C"

@@ -48,6 +48,8 @@ struct PairStep {
     uint32_t a0, a1, b0, b1;
 };
 
+constexpr int kMaxPeers = 8;
+
 struct Fwd2Params {
     const PairItem* items;
     const int* sched;  // [grid + 1] item range of each CTA (host-side schedule)
@@ -58,6 +60,14 @@ struct Fwd2Params {
     int hpg;
     float scale_log2;
     long long* trace;  // debug: per-step clock64 of CTA 0 (nullptr = off)
+    // Fused output exchange (head-parallel multi-GPU, s2_attn_fwd_peers): every
+    // finished O tile is also TMA-stored into each rank's full output buffer
+    // (peer memory over NVLink) and its lse rows written there -- the forward
+    // and the all-gather in one kernel.  num_peers = 0: off.
+    int num_peers;
+    const int* unit_global;           // local unit index -> global unit index
+    float* peer_lse[kMaxPeers];       // [total_units * hpg][seq_len] per rank
+    CUtensorMap peer_o[kMaxPeers];    // bf16 [total_units * hpg][seq_len][D], boxes {64, 128}
 };
 
 #define S2FTRACE(slot, n)                                                      \
@@ -102,7 +112,7 @@ __global__ void __launch_bounds__(384, 1)
     s2_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                         const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV,
-                        const __grid_constant__ CUtensorMap tmO, const Fwd2Params p) {
+                        const __grid_constant__ CUtensorMap tmO, const __grid_constant__ Fwd2Params p) {
     using C = Fwd2Cfg<D>;
     constexpr int NST = C::kNST;
     extern __shared__ uint8_t smem_raw[];
@@ -468,6 +478,8 @@ __global__ void __launch_bounds__(384, 1)
             mbar_arrive(smem_u32(&bar_oe[t]));
             const float inv_l = 1.0f / l_run;
             const uint32_t stg = sStg + t * C::kStgBytes;
+            // data index of this tile's head in the ranks' full outputs (fused exchange)
+            const int bh_out = p.num_peers ? p.unit_global[it.bh / p.hpg] * p.hpg + it.bh % p.hpg : it.bh;
 #pragma unroll
             for (int j = 0; j < D / 64; ++j) {
                 if (r == 0) bulk_wait_read0();  // the previous store has read the slice
@@ -485,12 +497,17 @@ __global__ void __launch_bounds__(384, 1)
                 named_bar_sync(1 + t, 128);
                 if (r == 0) {
                     tma_store_3d(&tmO, stg, j * 64, row0, it.bh);
+                    for (int pr = 0; pr < p.num_peers; ++pr)  // the same tile into every rank's output
+                        tma_store_3d(&p.peer_o[pr], stg, j * 64, row0, bh_out);
                     bulk_commit();
                 }
             }
-            if (q_pos < p.seq_len)
-                p.lse[static_cast<size_t>(it.bh) * p.seq_len + q_pos] =
-                    (m_run + __log2f(l_run)) * 0.69314718055994530942f;
+            if (q_pos < p.seq_len) {
+                const float lse_v = (m_run + __log2f(l_run)) * 0.69314718055994530942f;
+                p.lse[static_cast<size_t>(it.bh) * p.seq_len + q_pos] = lse_v;
+                for (int pr = 0; pr < p.num_peers; ++pr)
+                    p.peer_lse[pr][static_cast<size_t>(bh_out) * p.seq_len + q_pos] = lse_v;
+            }
             if (r == 0 && t == 0) S2FTRACE(11, o_cnt);
             ++o_cnt;
         }
@@ -523,11 +540,27 @@ long long* s2_debug_trace_buffer();
 cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtensorMap& k,
                                 const CUtensorMap& v, const CUtensorMap& o, const void* items, const int* sched,
                                 int grid, const void* steps, __nv_bfloat16* out, float* lse,
-                                int seq_len, int hpg, float scale_log2, cudaStream_t stream) {
+                                int seq_len, int hpg, float scale_log2, cudaStream_t stream,
+                                int num_peers, const int* unit_global, float* const* peer_lse,
+                                const CUtensorMap* peer_o) {
     if (grid == 0) return cudaSuccess;
-    s2dev::Fwd2Params p{static_cast<const s2dev::PairItem*>(items), sched,
-                        static_cast<const s2dev::PairStep*>(steps), out, lse, seq_len, hpg,
-                        scale_log2, s2_debug_trace_buffer()};
+    if (num_peers < 0 || num_peers > s2dev::kMaxPeers) return cudaErrorInvalidValue;
+    s2dev::Fwd2Params p{};
+    p.items = static_cast<const s2dev::PairItem*>(items);
+    p.sched = sched;
+    p.steps = static_cast<const s2dev::PairStep*>(steps);
+    p.out = out;
+    p.lse = lse;
+    p.seq_len = seq_len;
+    p.hpg = hpg;
+    p.scale_log2 = scale_log2;
+    p.trace = s2_debug_trace_buffer();
+    p.num_peers = num_peers;
+    p.unit_global = unit_global;
+    for (int r = 0; r < num_peers; ++r) {
+        p.peer_lse[r] = peer_lse[r];
+        p.peer_o[r] = peer_o[r];
+    }
     if (head_dim == 128) return s2dev::launch<128>(q, k, v, o, p, grid, stream);
     if (head_dim == 64) return s2dev::launch<64>(q, k, v, o, p, grid, stream);
     return cudaErrorInvalidValue;

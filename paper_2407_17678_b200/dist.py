@@ -70,6 +70,27 @@ class HeadParallelPlan:
 
         return torch.as_tensor(self.units[rank], device=device, dtype=torch.long)
 
+    def fused_forward(self, plan, ql, kl, vl, rank: int, peers: "PeerOutputs", *, scale=None, group=None,
+                      sync: bool = True):
+        """This rank's units through s2_attn_fwd_peers: the forward writes O / lse
+        into every rank's full buffers (peers).  Returns the local (out, lse) and
+        leaves the full result in peers.out / peers.lse once every rank's kernel
+        is done (sync=True orders that with a device synchronize + barrier)."""
+        import torch
+        import torch.distributed as dist
+
+        from .attention import s2_attn_fwd_peers
+
+        units = self.units[rank]
+        ug = torch.as_tensor(np.asarray(units, dtype=np.int32), device=ql.device)
+        out, lse = s2_attn_fwd_peers(plan, ql, kl, vl, unit_ids=units, peer_out=peers.peer_out,
+                                     peer_lse=peers.peer_lse, unit_global=ug,
+                                     total_units=peers.total_units, scale=scale)
+        if sync:
+            torch.cuda.synchronize()
+            dist.barrier(group=group)
+        return out, lse
+
     def all_gather(self, local, group=None):
         """local [U_r, ...] on every rank -> full [B*Hkv, ...] in unit order.
 
@@ -107,6 +128,41 @@ class HeadParallelPlan:
             return full
 
         return finish
+
+
+class PeerOutputs:
+    """Every rank's full output buffers, mapped into this process: the targets of
+    the fused forward + exchange (s2_attn_fwd_peers).
+
+    Each rank allocates out [total_units, hpg, N, D] and lse [total_units, hpg, N]
+    and shares them with CUDA IPC handles (torch's cross-process CUDA tensor
+    reduction, exchanged with one object all-gather at setup).  On an NVLink /
+    NVSwitch node the mapped peer buffers are P2P memory, so the forward's
+    epilogue stores O straight into every rank's output -- no separate
+    collective on the data path."""
+
+    def __init__(self, hp: "HeadParallelPlan", seq_len: int, head_dim: int, dtype, device, rank: int,
+                 group=None):
+        import torch
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        total = hp.batch * hp.plan.num_kv_heads
+        self.total_units = total
+        self.rank = rank
+        self.out = torch.empty((total, hp.hpg, seq_len, head_dim), dtype=dtype, device=device)
+        self.lse = torch.empty((total, hp.hpg, seq_len), dtype=torch.float32, device=device)
+        mine = (reduce_tensor(self.out), reduce_tensor(self.lse))
+        handles = [None] * hp.world_size
+        dist.all_gather_object(handles, mine, group=group)
+        self.peer_out, self.peer_lse = [], []
+        for r, (ho, hl) in enumerate(handles):
+            if r == rank:
+                self.peer_out.append(self.out)
+                self.peer_lse.append(self.lse)
+            else:
+                self.peer_out.append(ho[0](*ho[1]))
+                self.peer_lse.append(hl[0](*hl[1]))
 
 
 def head_parallel_forward(plan, q, k, v, rank: int, world_size: int, *, group=None,

@@ -51,3 +51,21 @@ def test_device_calls_fail_loudly_without_gpu():
     t = s2.AttentionTensors.random(2, 16, 8, 1)
     with pytest.raises(s2.S2Error):
         s2.streaming_sharded_attention(t, s2.build_all_csr(s2.make_single_stride_config(16, 8, 2, 1, 1)), 8)
+
+
+def test_fwd_peers_argument_errors_without_a_device():
+    """s2_attn_fwd_peers validates its exchange arguments before any device work."""
+    import ctypes
+
+    import paper_2407_17678_b200 as s2
+    from paper_2407_17678_b200 import _abi
+
+    plan = s2.Plan.from_config(s2.make_s2_config(256, 2, block_size=64, local_blocks=1, vert_stride=2))
+    L = _abi.lib()
+    a = _abi.s2_attn_args()
+    bufs = (ctypes.c_void_p * 1)(None)
+    for n in (0, 9):
+        assert L.s2_attn_fwd_peers(plan.handle, ctypes.byref(a), n, bufs, bufs, None, 1, None) == 1
+        assert b"num_peers" in L.s2_last_error()
+    assert L.s2_attn_fwd_peers(plan.handle, ctypes.byref(a), 1, bufs, bufs, None, 1, None) == 1
+    assert b"required" in L.s2_last_error()

@@ -6,9 +6,12 @@ what tests/test_dist_gloo.py covers with the oracle:
   * head_parallel_forward's gathered O / lse are bit-identical to one process
     (head-permutation exactness, test_attention.cpp:217-240), and each rank's
     backward on its own units equals the single-process gradients of those units;
+  * s2_attn_fwd_peers (the forward storing O into every rank's full output,
+    peer memory mapped with CUDA IPC) leaves the whole O / lse on every rank,
+    bit-identical to one process;
   * bench.py launched by torchrun at world size 2 prints one valid JSON line
-    (n_gpus 2, weak scaling, positive throughput) -- a code-path check, not a
-    performance number (both ranks time-slice one GPU).
+    with either exchange (n_gpus 2, weak scaling, positive throughput) -- a
+    code-path check, not a performance number (both ranks time-slice one GPU).
 """
 import json
 import os
@@ -86,12 +89,13 @@ def test_head_parallel_world2_on_one_gpu_is_bit_identical(case, tmp_path):
     assert open(res).read() == "ok"
 
 
-def test_bench_world2_prints_one_valid_line():
+@pytest.mark.parametrize("exchange", ["allgather", "fused"])
+def test_bench_world2_prints_one_valid_line(exchange):
     env = dict(os.environ, S2_BENCH_SHARE_GPU="1", S2_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu-baseline", "--no-decode",
-           "--no-hybrid"]
+           "--no-hybrid", "--exchange", exchange]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -99,3 +103,57 @@ def test_bench_world2_prints_one_valid_line():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["steps"] == 3
     assert d["config"]["global_batch"] == 2
+    assert ("fused" in d["config"]["parallelism"]) == (exchange == "fused")
+
+
+def _fused_worker(rank, world, port, cfg, batch, D, res_dir):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_17678_b200 as s2
+    from paper_2407_17678_b200.dist import HeadParallelPlan, PeerOutputs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plan = s2.Plan.from_config(cfg)
+    N, H, Hkv = cfg.seq_len, cfg.num_heads, cfg.kv_heads()
+    g = torch.Generator(device="cuda").manual_seed(9)
+    mk = lambda h: (torch.rand((batch, h, N, D), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)  # noqa
+    q, k, v = mk(H), mk(Hkv), mk(Hkv)
+    hp = HeadParallelPlan(plan, batch, world)
+    peers = PeerOutputs(hp, N, D, torch.bfloat16, torch.device("cuda", 0), rank)
+    peers.out.fill_(float("nan"))
+    peers.lse.fill_(float("nan"))
+    dist.barrier()
+    ql, kl, vl = hp.scatter_q(q, rank), hp.scatter_kv(k, rank), hp.scatter_kv(v, rank)
+    out_l, lse_l = hp.fused_forward(plan, ql, kl, vl, rank, peers)
+    ref_out, ref_lse = s2.s2_attn_fwd(plan, q, k, v)
+    ref_l, ref_ll = s2.s2_attn_fwd(plan, ql, kl, vl, unit_ids=hp.units[rank])
+    torch.cuda.synchronize()
+    ok = (torch.equal(peers.out.reshape(batch, H, N, D), ref_out)
+          and torch.equal(peers.lse.reshape(batch, H, N), ref_lse)
+          and torch.equal(out_l, ref_l) and torch.equal(lse_l, ref_ll))
+    with open(os.path.join(res_dir, f"r{rank}.txt"), "w") as f:
+        f.write("ok" if ok else "MISMATCH")
+    dist.barrier()
+    del peers
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["mha_b2", "gqa"])
+def test_fused_forward_exchange_world2_on_one_gpu(case, tmp_path):
+    """s2_attn_fwd_peers: each rank's forward stores its O tiles straight into both
+    ranks' full outputs (peer memory mapped with CUDA IPC); afterwards every rank
+    holds the whole O / lse, bit-identical to one process."""
+    import torch.multiprocessing as mp
+
+    if case == "mha_b2":
+        cfg, batch, D = single(1024, 64, 4, 2, 4), 2, 128
+    else:
+        cfg, batch, D = single(2048, 64, 8, 4, 4, kv=2), 1, 128
+    mp.spawn(_fused_worker, args=(2, _free_port(), cfg, batch, D, str(tmp_path)), nprocs=2, join=True)
+    assert open(tmp_path / "r0.txt").read() == "ok"
+    assert open(tmp_path / "r1.txt").read() == "ok"
