@@ -198,6 +198,8 @@ def lib():
                 f"`make -C paper_2407_17678_b200/csrc` (there is no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("S2ATTN_VARIANT") and not hasattr(L, name):
+                continue  # a tuning build of an older tree may predate a symbol
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

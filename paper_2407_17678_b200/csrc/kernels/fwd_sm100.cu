@@ -31,6 +31,8 @@
 // of a chunk overwrites the first 32 columns of its half as bf16x2), O at +128.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "sm100_ptx.cuh"
 
@@ -60,14 +62,26 @@ struct Fwd2Params {
     int hpg;
     float scale_log2;
     long long* trace;  // debug: per-step clock64 of CTA 0 (nullptr = off)
-    // Fused output exchange (head-parallel multi-GPU, s2_attn_fwd_peers): every
-    // finished O tile is also TMA-stored into each rank's full output buffer
-    // (peer memory over NVLink) and its lse rows written there -- the forward
-    // and the all-gather in one kernel.  num_peers = 0: off.
+};
+
+// Fused output exchange (head-parallel multi-GPU, s2_attn_fwd_peers): every
+// finished O tile is also TMA-stored into each rank's full output buffer (peer
+// memory over NVLink) and its lse rows written there -- the forward and the
+// all-gather in one kernel.  num_peers = 0: off.  A separate __grid_constant__
+// parameter: folding it into Fwd2Params (2.6 KB, all grid-constant) cost the
+// forward ~10%.
+struct FwdPeers {
     int num_peers;
     const int* unit_global;           // local unit index -> global unit index
     float* peer_lse[kMaxPeers];       // [total_units * hpg][seq_len] per rank
     CUtensorMap peer_o[kMaxPeers];    // bf16 [total_units * hpg][seq_len][D], boxes {64, 128}
+};
+// the plain forward's instantiation carries no exchange parameters at all
+struct NoPeers {
+    static constexpr int num_peers = 0;
+    const int* unit_global;
+    float* peer_lse[1];
+    CUtensorMap peer_o[1];
 };
 
 #define S2FTRACE(slot, n)                                                      \
@@ -107,12 +121,13 @@ __device__ __forceinline__ void apply_mask(float* s, int chunk, uint32_t mask, i
     }
 }
 
-template <int D>
+template <int D, bool PEERS>
 __global__ void __launch_bounds__(384, 1)
     s2_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                         const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV,
-                        const __grid_constant__ CUtensorMap tmO, const __grid_constant__ Fwd2Params p) {
+                        const __grid_constant__ CUtensorMap tmO, const Fwd2Params p,
+                        const __grid_constant__ std::conditional_t<PEERS, FwdPeers, NoPeers> px) {
     using C = Fwd2Cfg<D>;
     constexpr int NST = C::kNST;
     extern __shared__ uint8_t smem_raw[];
@@ -479,7 +494,7 @@ __global__ void __launch_bounds__(384, 1)
             const float inv_l = 1.0f / l_run;
             const uint32_t stg = sStg + t * C::kStgBytes;
             // data index of this tile's head in the ranks' full outputs (fused exchange)
-            const int bh_out = p.num_peers ? p.unit_global[it.bh / p.hpg] * p.hpg + it.bh % p.hpg : it.bh;
+            const int bh_out = px.num_peers ? px.unit_global[it.bh / p.hpg] * p.hpg + it.bh % p.hpg : it.bh;
 #pragma unroll
             for (int j = 0; j < D / 64; ++j) {
                 if (r == 0) bulk_wait_read0();  // the previous store has read the slice
@@ -497,16 +512,16 @@ __global__ void __launch_bounds__(384, 1)
                 named_bar_sync(1 + t, 128);
                 if (r == 0) {
                     tma_store_3d(&tmO, stg, j * 64, row0, it.bh);
-                    for (int pr = 0; pr < p.num_peers; ++pr)  // the same tile into every rank's output
-                        tma_store_3d(&p.peer_o[pr], stg, j * 64, row0, bh_out);
+                    for (int pr = 0; pr < px.num_peers; ++pr)  // the same tile into every rank's output
+                        tma_store_3d(&px.peer_o[pr], stg, j * 64, row0, bh_out);
                     bulk_commit();
                 }
             }
             if (q_pos < p.seq_len) {
                 const float lse_v = (m_run + __log2f(l_run)) * 0.69314718055994530942f;
                 p.lse[static_cast<size_t>(it.bh) * p.seq_len + q_pos] = lse_v;
-                for (int pr = 0; pr < p.num_peers; ++pr)
-                    p.peer_lse[pr][static_cast<size_t>(bh_out) * p.seq_len + q_pos] = lse_v;
+                for (int pr = 0; pr < px.num_peers; ++pr)
+                    px.peer_lse[pr][static_cast<size_t>(bh_out) * p.seq_len + q_pos] = lse_v;
             }
             if (r == 0 && t == 0) S2FTRACE(11, o_cnt);
             ++o_cnt;
@@ -524,12 +539,21 @@ __global__ void __launch_bounds__(384, 1)
 
 template <int D>
 static cudaError_t launch(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                          const CUtensorMap& o, const Fwd2Params& p, int grid, cudaStream_t stream) {
-    auto kern = s2_fwd_sm100_kernel<D>;
+                          const CUtensorMap& o, const Fwd2Params& p, const FwdPeers& px, int grid,
+                          cudaStream_t stream) {
+    if (px.num_peers == 0) {
+        auto kern = s2_fwd_sm100_kernel<D, false>;
+        cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::kSmem);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, 384, Fwd2Cfg<D>::kSmem, stream>>>(q, k, v, o, p, NoPeers{});
+        return cudaGetLastError();
+    }
+    auto kern = s2_fwd_sm100_kernel<D, true>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::kSmem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 384, Fwd2Cfg<D>::kSmem, stream>>>(q, k, v, o, p);
+    kern<<<grid, 384, Fwd2Cfg<D>::kSmem, stream>>>(q, k, v, o, p, px);
     return cudaGetLastError();
 }
 
@@ -545,23 +569,17 @@ cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtens
                                 const CUtensorMap* peer_o) {
     if (grid == 0) return cudaSuccess;
     if (num_peers < 0 || num_peers > s2dev::kMaxPeers) return cudaErrorInvalidValue;
-    s2dev::Fwd2Params p{};
-    p.items = static_cast<const s2dev::PairItem*>(items);
-    p.sched = sched;
-    p.steps = static_cast<const s2dev::PairStep*>(steps);
-    p.out = out;
-    p.lse = lse;
-    p.seq_len = seq_len;
-    p.hpg = hpg;
-    p.scale_log2 = scale_log2;
-    p.trace = s2_debug_trace_buffer();
-    p.num_peers = num_peers;
-    p.unit_global = unit_global;
+    s2dev::Fwd2Params p{static_cast<const s2dev::PairItem*>(items), sched,
+                        static_cast<const s2dev::PairStep*>(steps), out, lse, seq_len, hpg,
+                        scale_log2, s2_debug_trace_buffer()};
+    s2dev::FwdPeers px{};
+    px.num_peers = num_peers;
+    px.unit_global = unit_global;
     for (int r = 0; r < num_peers; ++r) {
-        p.peer_lse[r] = peer_lse[r];
-        p.peer_o[r] = peer_o[r];
+        px.peer_lse[r] = peer_lse[r];
+        px.peer_o[r] = peer_o[r];
     }
-    if (head_dim == 128) return s2dev::launch<128>(q, k, v, o, p, grid, stream);
-    if (head_dim == 64) return s2dev::launch<64>(q, k, v, o, p, grid, stream);
+    if (head_dim == 128) return s2dev::launch<128>(q, k, v, o, p, px, grid, stream);
+    if (head_dim == 64) return s2dev::launch<64>(q, k, v, o, p, px, grid, stream);
     return cudaErrorInvalidValue;
 }
