@@ -1,0 +1,110 @@
+"""The reference's numerics pins (test_attention.cpp) on the bf16
+tcgen05 path -- forward AND backward -- where they hold exactly:
+
+* N = 1 (test_attention.cpp:72-79): out == v bit-for-bit; the only weight is 1,
+  so dS = P (dP - delta) = 0 algebraically -- in fp32 dP (tensor-core dot) and
+  delta (the prep kernel's row sum) round differently, so dQ, dK are ~1e-8,
+  not bit-zero -- and dV == dO.
+* v == 0 (:81-87): out == 0 exactly, lse finite.
+* N < block (:149-156) and a ragged N (:284-294): parity with the oracle.
+* Unattended V rows perturbed by +1000 (:196-215): out unchanged bit-for-bit,
+  and so are dQ / dK; only those rows' dV may differ (and must stay 0).
+"""
+import numpy as np
+import pytest
+
+import paper_2407_17678_b200 as s2
+import helpers  # noqa: F401  (puts oracle/ on sys.path)
+from helpers import bf16_round, single
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(x, shape):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).reshape(shape).to("cuda", torch.bfloat16)
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_single_token_is_exact(D):
+    import torch
+
+    cfg = single(1, 64, 4, 1, 2)
+    plan = s2.Plan.from_config(cfg)
+    rng = np.random.default_rng(1)
+    q, k, v, do = (_t(rng.uniform(-1, 1, 4 * D), (1, 4, 1, D)) for _ in range(4))
+    out, lse = s2.s2_attn_fwd(plan, q, k, v)
+    dq, dk, dv = s2.s2_attn_bwd(plan, q, k, v, out, lse, do)
+    torch.cuda.synchronize()
+    assert torch.equal(out, v)
+    assert float(dq.abs().max()) <= 1e-5 and float(dk.abs().max()) <= 1e-5
+    torch.testing.assert_close(dv.float(), do.float(), rtol=1e-2, atol=1e-6)
+    # lse = scale * q.k (one key)
+    ref = (q.float() * k.float()).sum(-1) / np.sqrt(D)
+    torch.testing.assert_close(lse, ref, rtol=1e-5, atol=1e-5)
+
+
+def test_zero_values_give_zero_output():
+    import torch
+
+    cfg = single(1000, 64, 4, 2, 4)
+    plan = s2.Plan.from_config(cfg)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    q = (torch.rand(1, 4, 1000, 128, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    k = (torch.rand(1, 4, 1000, 128, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    v = torch.zeros_like(k)
+    out, lse = s2.s2_attn_fwd(plan, q, k, v)
+    torch.cuda.synchronize()
+    assert torch.all(out == 0)
+    assert torch.all(torch.isfinite(lse))
+
+
+@pytest.mark.parametrize("N,S,local,vs", [(30, 64, 1, 2), (45, 16, 2, 3), (130, 64, 2, 2)])
+def test_short_and_ragged_sequences_match_oracle(N, S, local, vs):
+    cfg = single(N, S, 2, local, vs)
+    plan = s2.Plan.from_config(cfg)
+    rng = np.random.default_rng(N)
+    q, k, v, do = (bf16_round(rng.uniform(-1, 1, 2 * N * 128).astype(np.float32)) for _ in range(4))
+    shape = (1, 2, N, 128)  # (the fp32 path covers blocks that are not multiples of 16)
+    tq, tk, tv, tdo = (_t(x, shape) for x in (q, k, v, do))
+    out, lse = s2.s2_attn_fwd(plan, tq, tk, tv)
+    dq, dk, dv = s2.s2_attn_bwd(plan, tq, tk, tv, out, lse, tdo)
+    rp, ci = oracle.csr_all(cfg)
+    ro, rl = oracle.attn_fwd(q, k, v, rp, ci, 1, 2, 2, N, 128, S)
+    rq, rk, rv = oracle.attn_bwd(q, k, v, do, rp, ci, 1, 2, 2, N, 128, S)
+    f = lambda t: t.float().cpu().numpy().ravel()  # noqa: E731
+    np.testing.assert_allclose(f(out), ro, rtol=1e-2, atol=1e-2)
+    np.testing.assert_allclose(lse.cpu().numpy().ravel(), rl, rtol=1e-2, atol=1e-2)
+    for g_, r_ in ((dq, rq), (dk, rk), (dv, rv)):
+        np.testing.assert_allclose(f(g_), r_, rtol=1e-2, atol=1e-2)
+
+
+def test_unattended_value_rows_change_nothing_fwd_and_bwd():
+    """A hand-made CSR whose key blocks 5..7 no row attends (rows 5..7 list only
+    block 0, every other row {0, i}): V rows there perturbed by +1000 change no
+    output, no lse and no gradient except nothing (their dV rows stay 0)."""
+    import torch
+
+    from paper_2407_17678_b200.pattern import CsrMask
+
+    N, H, S = 1024, 2, 64
+    B = N // S
+    rows = [[0] if i in (5, 6, 7) else sorted({0, i}) for i in range(B)]
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int32)
+    ci = np.concatenate(rows).astype(np.int32)
+    plan = s2.Plan.from_csr([CsrMask(h, B, rp, ci) for h in range(H)], N, S)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    mk = lambda: (torch.rand(1, H, N, 128, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)  # noqa
+    q, k, v, do = mk(), mk(), mk(), mk()
+    v2 = v.clone()
+    v2[:, :, 5 * S:8 * S] += 1000
+    out, lse = s2.s2_attn_fwd(plan, q, k, v)
+    out2, lse2 = s2.s2_attn_fwd(plan, q, k, v2)
+    dq, dk, dv = s2.s2_attn_bwd(plan, q, k, v, out, lse, do)
+    dq2, dk2, dv2 = s2.s2_attn_bwd(plan, q, k, v2, out2, lse2, do)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2) and torch.equal(lse, lse2)
+    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
+    assert torch.all(dv[:, :, 5 * S:8 * S] == 0) and torch.all(dk[:, :, 5 * S:8 * S] == 0)
