@@ -81,7 +81,9 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
         const CUtensorMap do128 = make_map_bf16_3d(a->dout, D, N, nqbh, 64, 128);
         const CUtensorMap mk = make_map_bf16_3d(f.k, D, N, nkv, 64, 64);
         const CUtensorMap mv = make_map_bf16_3d(f.v, D, N, nkv, 64, 64);
-        if (w->bwd_dropped) {  // tiles without attending queries are not visited: their dK/dV are 0
+        // key chunks no query attends are never visited (no tile covers them, or a
+        // tile has no steps): their dK / dV are 0
+        if (w->bwd_dropped || L->bwd.uncovered) {
             const size_t bytes = static_cast<size_t>(nkv) * N * D * 2;
             if ((e = cudaMemsetAsync(a->dk, 0, bytes, st)) != cudaSuccess ||
                 (e = cudaMemsetAsync(a->dv, 0, bytes, st)) != cudaSuccess)

@@ -95,6 +95,13 @@ struct Fwd2Cfg {
     static constexpr int kSub = D / 64;
     static constexpr int kQBytes = kSub * 16384;  // 128 rows
     static constexpr int kCBytes = kSub * 8192;   // one 64-key chunk of K (or V)
+// exp2 on the FMA pipe (cubic) for 1 in (mask+1) pairs; -1: all on MUFU.EX2.
+// With separate S / P V issuers the MUFU pipe no longer paces the softmax, and
+// emulation only adds instructions (same-box A/B: 25% 0.784 ms, 12.5% 0.760 ms,
+// 0% 0.748 ms).
+#ifndef S2_FWD_POLY_MASK
+#define S2_FWD_POLY_MASK -1
+#endif
 #ifndef S2_FWD_NST
 #define S2_FWD_NST 4
 #endif
@@ -452,7 +459,7 @@ __global__ void __launch_bounds__(384, 1)
                         for (int j = 0; j < 16; ++j) {
                             const uint64_t x = ffma2(f2_pack(sv[c * 32 + 2 * j], sv[c * 32 + 2 * j + 1]), sl2v, nbase);
                             uint64_t pr;
-                            if ((j & 3) == 3) {
+                            if (S2_FWD_POLY_MASK >= 0 && (j & S2_FWD_POLY_MASK) == S2_FWD_POLY_MASK) {  // 1 in (mask+1) on the FMA pipe
                                 pr = exp2_poly2(x);
                             } else {
                                 float x0, x1;

@@ -268,8 +268,12 @@ BwdList build_bwd_list(const FwdList& fwd, int num_heads, int num_kv_heads, int 
                 lists[fwd.chunks[e].chunk].push_back({t, fwd.chunks[e].mask});
         }
         std::vector<int> order;
-        for (int c = 0; c < nchunks; ++c)
-            if (!lists[c].empty()) order.push_back(c);
+        for (int c = 0; c < nchunks; ++c) {
+            if (!lists[c].empty())
+                order.push_back(c);
+            else
+                b.uncovered = true;  // no tile will write this chunk's dK / dV
+        }
         std::sort(order.begin(), order.end(), [&](int a, int c) {
             if (lists[a].size() != lists[c].size()) return lists[a].size() > lists[c].size();
             if (lists[a][0].t != lists[c][0].t) return lists[a][0].t < lists[c][0].t;

@@ -111,6 +111,9 @@ struct BwdEntry {
 struct BwdList {
     std::vector<BwdTile> tiles;
     std::vector<BwdEntry> entries;
+    // some 64-key chunk of some kv group has no attending query, so no tile
+    // covers it: its dK / dV are 0 and must be written as such (zero-filled)
+    bool uncovered = false;
 };
 BwdList build_bwd_list(const FwdList& fwd, int num_heads, int num_kv_heads, int seq_len);
 

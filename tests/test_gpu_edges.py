@@ -84,7 +84,9 @@ def test_short_and_ragged_sequences_match_oracle(N, S, local, vs):
 def test_unattended_value_rows_change_nothing_fwd_and_bwd():
     """A hand-made CSR whose key blocks 5..7 no row attends (rows 5..7 list only
     block 0, every other row {0, i}): V rows there perturbed by +1000 change no
-    output, no lse and no gradient except nothing (their dV rows stay 0)."""
+    output, lse or gradient; their dK / dV rows are exactly 0 (no tile covers
+    those chunks: the backward zero-fills them -- found by this test when the
+    output buffers held stale data)."""
     import torch
 
     from paper_2407_17678_b200.pattern import CsrMask
