@@ -498,7 +498,9 @@ __global__ void __launch_bounds__(384, 1)
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(smem_u32(&bar_oe[t]));
-            const float inv_l = 1.0f / l_run;
+            // a row with no admitted key: out = 0/0 = NaN, lse = -inf (the reference's
+            // acc / l); explicit, since a tile without any chunk never wrote its O
+            const float inv_l = l_run > 0.f ? 1.0f / l_run : __int_as_float(0x7fc00000);
             const uint32_t stg = sStg + t * C::kStgBytes;
             // data index of this tile's head in the ranks' full outputs (fused exchange)
             const int bh_out = px.num_peers ? px.unit_global[it.bh / p.hpg] * p.hpg + it.bh % p.hpg : it.bh;

@@ -110,3 +110,28 @@ def test_unattended_value_rows_change_nothing_fwd_and_bwd():
     assert torch.equal(out, out2) and torch.equal(lse, lse2)
     assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
     assert torch.all(dv[:, :, 5 * S:8 * S] == 0) and torch.all(dk[:, :, 5 * S:8 * S] == 0)
+
+
+def test_rows_without_keys_follow_the_reference():
+    """A CSR row block that lists no key block: the reference yields out = 0/0 = NaN
+    and lse = -inf for its rows (acc / l with nothing admitted); so do the kernels,
+    whether the 128-row tile has other attended rows or none at all."""
+    import torch
+
+    from paper_2407_17678_b200.pattern import CsrMask
+
+    N, H, S, D = 512, 2, 64, 128
+    B = N // S
+    rows = [[0], [0, 1], [], [0, 3], [], [], [0, 6], [6, 7]]  # tile 2 (blocks 4, 5) has no key at all
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int32)
+    ci = np.concatenate([np.array(r, np.int32) for r in rows]).astype(np.int32)
+    plan = s2.Plan.from_csr([CsrMask(h, B, rp, ci) for h in range(H)], N, S)
+    rng = np.random.default_rng(4)
+    q, k, v = (bf16_round(rng.uniform(-1, 1, H * N * D).astype(np.float32)) for _ in range(3))
+    out, lse = s2.s2_attn_fwd(plan, *(_t(x, (1, H, N, D)) for x in (q, k, v)))
+    torch.cuda.synchronize()
+    ro, rl = oracle.attn_fwd(q, k, v, np.tile(rp, H), np.tile(ci, H), 1, H, H, N, D, S)
+    o = out.float().cpu().numpy().ravel()
+    np.testing.assert_allclose(o, ro, rtol=1e-2, atol=1e-2, equal_nan=True)
+    np.testing.assert_allclose(lse.cpu().numpy().ravel(), rl, rtol=1e-2, atol=1e-2, equal_nan=True)
+    assert np.isnan(ro).any() and np.array_equal(np.isnan(o), np.isnan(ro))
