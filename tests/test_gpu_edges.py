@@ -135,3 +135,14 @@ def test_rows_without_keys_follow_the_reference():
     np.testing.assert_allclose(o, ro, rtol=1e-2, atol=1e-2, equal_nan=True)
     np.testing.assert_allclose(lse.cpu().numpy().ravel(), rl, rtol=1e-2, atol=1e-2, equal_nan=True)
     assert np.isnan(ro).any() and np.array_equal(np.isnan(o), np.isnan(ro))
+    # backward: those rows admit no key, so they contribute nothing (dQ rows 0,
+    # no dK / dV terms) even though their lse is -inf and their O is NaN
+    do = bf16_round(rng.uniform(-1, 1, H * N * D).astype(np.float32))
+    tq, tk, tv, tdo = (_t(x, (1, H, N, D)) for x in (q, k, v, do))
+    dq, dk, dv = s2.s2_attn_bwd(plan, tq, tk, tv, out, lse, tdo)
+    torch.cuda.synchronize()
+    rq, rk, rv = oracle.attn_bwd(q, k, v, do, np.tile(rp, H), np.tile(ci, H), 1, H, H, N, D, S)
+    for g_, r_ in ((dq, rq), (dk, rk), (dv, rv)):
+        gg = g_.float().cpu().numpy().ravel()
+        assert np.isfinite(gg).all()
+        np.testing.assert_allclose(gg, r_, rtol=1e-2, atol=1e-2)
