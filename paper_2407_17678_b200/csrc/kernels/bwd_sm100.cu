@@ -640,7 +640,9 @@ __global__ void __launch_bounds__(384, 1)
             const int i_end = p.sched[blockIdx.x + 1];
             for (int i = p.sched[blockIdx.x]; i < i_end; ++i, ++it_cnt) {
                 const int chunk_cnt = warp_uniform(items[i].chunk_cnt);
+                S2TRACE(13, it_cnt);
                 mbar_wait(smem_u32(&bar_qf), it_cnt & 1);
+                S2TRACE(14, it_cnt);
                 if (leader) {  // after the previous item's last S / dP MMAs (issue order)
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {

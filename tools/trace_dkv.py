@@ -56,3 +56,8 @@ if ni > 2:
     e = t[:, 1:ni - 1].astype(np.float64)
     print(f"items traced {ni}: EW wait af {np.median(e[9] - e[8]):.0f}, epilogue {np.median(e[10] - e[9]):.0f}; "
           f"MMA wait ae {np.median(e[12] - e[11]):.0f}")
+
+ni2 = int((t[14] != -t0).sum())
+if ni2 > 3:
+    e = t[:, 1:ni2 - 1].astype(np.float64)
+    print(f"dq items traced {ni2}: MMA wait for the next item's Q/dO (bar_qf) median {np.median(e[14] - e[13]):.0f} cycles")
