@@ -136,6 +136,47 @@ def _require_cuda(*ts):
             raise _abi.S2InvalidArgument(1, "tensors must be contiguous")
 
 
+def _check_tensors(q, k, v, out=None, lse=None, dout=None, grads=(), unit_ids=None):
+    """Shapes / dtypes / devices the C ABI takes on trust (it receives pointers):
+    mismatches raise here instead of reading out of bounds (kernel_common.hpp:20-32's
+    size checks, for device tensors)."""
+    import torch
+
+    def bad(msg):
+        raise _abi.S2InvalidArgument(1, msg)
+
+    if q.dtype not in (torch.bfloat16, torch.float32):
+        bad("q must be bfloat16 or float32")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        bad("q, k and v must share one dtype")
+    if k.shape != v.shape:
+        bad("k and v shapes differ")
+    if unit_ids is None:
+        if q.dim() != 4 or k.dim() != 4:
+            bad("q must be [B, H, N, D] and k/v [B, Hkv, N, D]")
+        if k.shape[0] != q.shape[0] or k.shape[2] != q.shape[2] or k.shape[3] != q.shape[3]:
+            bad("q and k/v disagree in batch, seq_len or head_dim")
+    else:
+        if q.dim() != 4 or k.dim() != 3:
+            bad("with unit_ids, q must be [U, H/Hkv, N, D] and k/v [U, N, D]")
+        if k.shape[0] != q.shape[0] or k.shape[1] != q.shape[2] or k.shape[2] != q.shape[3]:
+            bad("q and k/v disagree in units, seq_len or head_dim")
+        if len(unit_ids) != q.shape[0]:
+            bad("len(unit_ids) must equal the packed unit dimension")
+    devs = {t.device for t in (q, k, v, out, lse, dout, *grads) if t is not None}
+    if len(devs) != 1:
+        bad("tensors live on different devices")
+    if out is not None and (out.shape != q.shape or out.dtype != q.dtype):
+        bad("out must have q's shape and dtype")
+    if lse is not None and (tuple(lse.shape) != tuple(q.shape[:-1]) or lse.dtype != torch.float32):
+        bad("lse must be float32 with q's shape without head_dim")
+    if dout is not None and (dout.shape != q.shape or dout.dtype != q.dtype):
+        bad("dout must have q's shape and dtype")
+    for g, ref in zip(grads, (q, k, v)):
+        if g is not None and (g.shape != ref.shape or g.dtype != ref.dtype):
+            bad("dq/dk/dv must have the shapes and dtype of q/k/v")
+
+
 def _fwd_args(plan, q, k, v, out, lse, scale, num_splits, unit_ids):
     if unit_ids is None:
         B, H, N, D = q.shape
@@ -176,6 +217,8 @@ def s2_attn_fwd(plan: Plan, q, k, v, *, scale: Optional[float] = None, num_split
         out = torch.empty_like(q)
     if lse is None:
         lse = torch.empty(q.shape[:-1], device=q.device, dtype=torch.float32)
+    _require_cuda(out, lse)
+    _check_tensors(q, k, v, out, lse, unit_ids=unit_ids)
     a, keep = _fwd_args(plan, q, k, v, out, lse, scale, num_splits, unit_ids)
     check(lib().s2_attn_fwd(plan.handle, ctypes.byref(a), _stream_ptr(stream)))
     return out, lse
@@ -197,6 +240,14 @@ def s2_attn_fwd_peers(plan: Plan, q, k, v, *, unit_ids, peer_out, peer_lse, unit
         out = torch.empty_like(q)
     if lse is None:
         lse = torch.empty(q.shape[:-1], device=q.device, dtype=torch.float32)
+    _require_cuda(out, lse)
+    _check_tensors(q, k, v, out, lse, unit_ids=unit_ids)
+    full = (int(total_units),) + tuple(q.shape[1:])
+    for po_, pl_ in zip(peer_out, peer_lse):
+        if tuple(po_.shape) != full or po_.dtype != q.dtype or tuple(pl_.shape) != full[:-1]:
+            raise _abi.S2InvalidArgument(1, "peer buffers must be [total_units, H/Hkv, N, D] / [.., N]")
+    if unit_global.numel() != q.shape[0]:
+        raise _abi.S2InvalidArgument(1, "unit_global must list one global unit per local unit")
     a, keep = _fwd_args(plan, q, k, v, out, lse, scale, 1, unit_ids)
     n = len(peer_out)
     if len(peer_lse) != n:
@@ -218,6 +269,8 @@ def s2_attn_bwd(plan: Plan, q, k, v, out, lse, dout, *, scale: Optional[float] =
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
+    _require_cuda(dq, dk, dv)
+    _check_tensors(q, k, v, out, lse, dout, (dq, dk, dv), unit_ids=unit_ids)
     fa, keep = _fwd_args(plan, q, k, v, out, lse, scale, 1, unit_ids)
     a = _abi.s2_attn_bwd_args()
     a.fwd = fa

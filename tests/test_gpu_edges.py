@@ -146,3 +146,27 @@ def test_rows_without_keys_follow_the_reference():
         gg = g_.float().cpu().numpy().ravel()
         assert np.isfinite(gg).all()
         np.testing.assert_allclose(gg, r_, rtol=1e-2, atol=1e-2)
+
+
+def test_tensor_contract_errors_raise_instead_of_reading_out_of_bounds():
+    import torch
+
+    plan = s2.Plan.from_config(single(256, 64, 4, 2, 2))
+    mk = lambda *sh, dt=torch.bfloat16: torch.zeros(*sh, device="cuda", dtype=dt)  # noqa: E731
+    q, k, v = mk(1, 4, 256, 128), mk(1, 4, 256, 128), mk(1, 4, 256, 128)
+    bad_cases = [
+        ((q, k, mk(1, 4, 128, 128)), {}),                        # v shape != k shape
+        ((q, k.float(), v.float()), {}),                          # dtype mismatch
+        ((q, mk(1, 4, 128, 128), mk(1, 4, 128, 128)), {}),        # seq_len mismatch
+        ((q, k, v), {"out": mk(1, 4, 256, 64)}),                  # out shape
+        ((q, k, v), {"lse": mk(1, 4, 256, dt=torch.bfloat16)}),   # lse dtype
+        ((q.transpose(2, 3), k, v), {}),                          # non-contiguous
+    ]
+    for args, kw in bad_cases:
+        with pytest.raises(s2.S2InvalidArgument):
+            s2.s2_attn_fwd(plan, *args, **kw)
+    out, lse = s2.s2_attn_fwd(plan, q, k, v)
+    with pytest.raises(s2.S2InvalidArgument):
+        s2.s2_attn_bwd(plan, q, k, v, out, lse, mk(1, 4, 128, 128))     # dout shape
+    with pytest.raises(s2.S2InvalidArgument):
+        s2.s2_attn_bwd(plan, q, k, v, out, lse, q, dk=mk(1, 4, 256, 64))  # dk shape
