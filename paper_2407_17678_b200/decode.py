@@ -59,11 +59,26 @@ class KVCache:
         check(lib().s2_attn_decode_bytes(self._h, ctypes.byref(n)))
         return n.value
 
+    def _check(self, what, want_shape, *ts):
+        """The C ABI reads these through raw pointers: shapes and dtype first."""
+        import torch
+
+        for t in ts:
+            if t.dtype != torch.bfloat16:
+                raise _abi.S2InvalidArgument(1, f"{what}: bfloat16 tensors required")
+            if tuple(t.shape) != tuple(want_shape):
+                raise _abi.S2InvalidArgument(1, f"{what}: expected shape {tuple(want_shape)}, got {tuple(t.shape)}")
+
     def prefill(self, k, v, stream=None):
         """k, v: [batch, Hkv, T, D] bf16 CUDA tensors (dense prefix)."""
         from .attention import _require_cuda, _stream_ptr
 
         _require_cuda(k, v)
+        if k.dim() != 4:
+            raise _abi.S2InvalidArgument(1, "prefill: k/v must be [batch, Hkv, T, D]")
+        if k.shape[2] > self.plan.seq_len:
+            raise _abi.S2InvalidArgument(1, "prefill: T exceeds the plan's seq_len (the cache capacity)")
+        self._check("prefill", (self.batch, self.plan.num_kv_heads, k.shape[2], self.head_dim), k, v)
         check(lib().s2_kvcache_prefill(self._h, ctypes.c_void_p(k.data_ptr()),
                                        ctypes.c_void_p(v.data_ptr()), k.shape[2],
                                        _stream_ptr(stream)))
@@ -73,6 +88,7 @@ class KVCache:
         from .attention import _require_cuda, _stream_ptr
 
         _require_cuda(k, v)
+        self._check("append", (self.batch, self.plan.num_kv_heads, self.head_dim), k, v)
         check(lib().s2_kvcache_append(self._h, ctypes.c_void_p(k.data_ptr()),
                                       ctypes.c_void_p(v.data_ptr()), _stream_ptr(stream)))
 
@@ -83,10 +99,15 @@ class KVCache:
         from .attention import _require_cuda, _stream_ptr
 
         _require_cuda(q)
+        self._check("decode", (self.batch, self.plan.num_heads, self.head_dim), q)
         if out is None:
             out = torch.empty_like(q)
         if lse is None:
             lse = torch.empty(q.shape[:2], device=q.device, dtype=torch.float32)
+        _require_cuda(out, lse)
+        self._check("decode out", tuple(q.shape), out)
+        if tuple(lse.shape) != tuple(q.shape[:2]) or lse.dtype != torch.float32:
+            raise _abi.S2InvalidArgument(1, "decode: lse must be float32 [batch, H]")
         if self._ws is None:
             self._ws = torch.empty(max(self._ws_bytes, 16), dtype=torch.uint8, device=q.device)
         check(lib().s2_attn_decode(self._h, ctypes.c_void_p(q.data_ptr()),

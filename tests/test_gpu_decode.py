@@ -87,3 +87,22 @@ def test_non_kv_efficient_mask_rejected():
     plan = s2.Plan.from_config(cfg)
     with pytest.raises(s2.S2Unsupported):
         KVCache(plan, 1, 128)
+
+
+def test_cache_tensor_contract_errors_raise():
+    import torch
+
+    cfg = single(1024, 64, 8, 2, 2, kv=2)
+    cache = KVCache(s2.Plan.from_config(cfg), 2, 128)
+    z = lambda *sh, dt=torch.bfloat16: torch.zeros(*sh, device="cuda", dtype=dt)  # noqa: E731
+    with pytest.raises(s2.S2InvalidArgument):
+        cache.prefill(z(2, 8, 10, 128), z(2, 8, 10, 128))      # query heads, not kv heads
+    with pytest.raises(s2.S2InvalidArgument):
+        cache.prefill(z(2, 2, 2000, 128), z(2, 2, 2000, 128))  # past the capacity
+    cache.prefill(z(2, 2, 10, 128), z(2, 2, 10, 128))
+    with pytest.raises(s2.S2InvalidArgument):
+        cache.append(z(2, 2, 64), z(2, 2, 64))                 # head_dim
+    with pytest.raises(s2.S2InvalidArgument):
+        cache.decode(z(2, 8, 128, dt=torch.float32))           # dtype
+    out, lse = cache.decode(z(2, 8, 128))
+    assert out.shape == (2, 8, 128) and lse.shape == (2, 8)
