@@ -29,6 +29,9 @@
 namespace s2dev {
 
 // ------------------------------------------------------------------ prep
+#ifndef S2_PREP_ROWS
+#define S2_PREP_ROWS 1
+#endif
 // Delta = rowsum(dO o O) and lse*log2(e) per row; HBM-bound (reads O and dO
 // once).  D/8 lanes own a row (16-byte loads), 256 / (D/8) rows per 256-thread
 // block iteration, grid-stride over rows.
@@ -39,30 +42,47 @@ __global__ void __launch_bounds__(256) s2_bwd_prep_kernel(const __nv_bfloat16* _
                                                           float* __restrict__ delta,
                                                           float* __restrict__ lse2, int num_bh,
                                                           int N, int Npad) {
+    // Rows in 32-bit arithmetic (the host checks num_bh * Npad < 2^31): a 64-bit
+    // divide / modulo per row made this kernel issue-bound, not HBM-bound.
     constexpr int LPR = D / 8;  // lanes per row
-    const long long total = static_cast<long long>(num_bh) * Npad;
-    const int sub = threadIdx.x % LPR;
-    for (long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / LPR; row < total;
-         row += static_cast<long long>(gridDim.x) * blockDim.x / LPR) {
-        const int bh = static_cast<int>(row / Npad), t = static_cast<int>(row % Npad);
-        float acc = 0.f;
-        if (t < N) {
-            const size_t off = (static_cast<size_t>(bh) * N + t) * D + sub * 8;
-            const uint4 a = __ldg(reinterpret_cast<const uint4*>(out + off));
-            const uint4 b = __ldg(reinterpret_cast<const uint4*>(dout + off));
-            const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+    constexpr int kRows = S2_PREP_ROWS;  // rows per thread per sweep (2 x kRows 16-byte loads in flight)
+    const uint32_t total = static_cast<uint32_t>(num_bh) * static_cast<uint32_t>(Npad);
+    const uint32_t sub = threadIdx.x % LPR;
+    const uint32_t stride = gridDim.x * blockDim.x / LPR;  // rows per sweep
+    for (uint32_t row0 = (blockIdx.x * blockDim.x + threadIdx.x) / LPR; row0 < total; row0 += kRows * stride) {
+        uint4 a[kRows], b[kRows];
+        uint32_t bh[kRows], t[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {  // issue every load first
+            const uint32_t row = row0 + u * stride;
+            bh[u] = row / static_cast<uint32_t>(Npad);
+            t[u] = row - bh[u] * static_cast<uint32_t>(Npad);
+            a[u] = b[u] = make_uint4(0u, 0u, 0u, 0u);
+            if (row < total && t[u] < static_cast<uint32_t>(N)) {
+                const size_t off = (static_cast<size_t>(bh[u]) * N + t[u]) * D + sub * 8;
+                a[u] = __ldg(reinterpret_cast<const uint4*>(out + off));
+                b[u] = __ldg(reinterpret_cast<const uint4*>(dout + off));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+            const uint32_t row = row0 + u * stride;
+            const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a[u]);
+            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b[u]);
+            float acc = 0.f;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const float2 x = __bfloat1622float2(a2[j]), y = __bfloat1622float2(b2[j]);
                 acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
             }
-        }
 #pragma unroll
-        for (int s = LPR / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-        if (sub == 0) {
-            delta[row] = acc;
-            lse2[row] = t < N ? lse[static_cast<size_t>(bh) * N + t] * 1.4426950408889634f : INFINITY;
+            for (int s = LPR / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+            if (sub == 0 && row < total) {
+                delta[row] = acc;
+                lse2[row] = t[u] < static_cast<uint32_t>(N)
+                                ? lse[static_cast<size_t>(bh[u]) * N + t[u]] * 1.4426950408889634f
+                                : INFINITY;
+            }
         }
     }
 }
@@ -823,6 +843,7 @@ cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* do
                                const float* lse, float* delta, float* lse2, int num_bh, int N,
                                int Npad, int D, cudaStream_t stream) {
     const long long rows = static_cast<long long>(num_bh) * Npad;
+    if (rows >= (1ll << 31)) return cudaErrorInvalidValue;  // the kernel indexes rows in 32 bits
     const int per_block = 256 / (D / 8);
     const long long need = (rows + per_block - 1) / per_block;
     const int blocks = static_cast<int>(std::min<long long>(need, 148LL * 8));
