@@ -42,6 +42,7 @@ CASES = {
     "cfg1_shape_d64": (single(2048, 64, 8, 4, 8), 1, 64),
     "batch2_h8_n2048": (single(2048, 64, 8, 4, 16), 2, 128),
     "gqa_16q4kv": (single(2048, 64, 16, 4, 4, kv=4), 1, 128),
+    "gqa_8q2kv_d64_batch2": (single(1536, 64, 8, 3, 4, kv=2), 2, 64),
     "block128": (single(1024, 128, 2, 2, 3), 1, 128),
     "block32_ragged": (single(900, 32, 2, 3, 5), 1, 128),
     "single_tile": (single(100, 64, 2, 1, 2), 1, 128),

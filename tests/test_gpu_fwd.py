@@ -57,6 +57,7 @@ BF16_CASES = {
     "h4_n1000_ragged_d128": (single(1000, 64, 4, 2, 4), 1, 128),
     "cfg2_like_batch2_n2048": (single(2048, 64, 32, 4, 16), 2, 128),
     "gqa_32q8kv": (single(2048, 64, 32, 4, 8, kv=8), 1, 128),
+    "gqa_8q2kv_d64_batch2": (single(1536, 64, 8, 3, 4, kv=2), 2, 64),
     "block128": (single(2048, 128, 4, 2, 3), 1, 128),
     "block32": (single(1536, 32, 4, 3, 5), 1, 64),
     "block16_local_stride2": (single(700, 16, 2, 5, 4, local_stride=2), 1, 128),
