@@ -106,3 +106,44 @@ def test_cache_tensor_contract_errors_raise():
         cache.decode(z(2, 8, 128, dt=torch.float32))           # dtype
     out, lse = cache.decode(z(2, 8, 128))
     assert out.shape == (2, 8, 128) and lse.shape == (2, 8)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_decode_fuzz_matches_oracle(seed):
+    """Seeded random KV-efficient configs (local_stride 1; the decode cache's
+    block 64 and 1/2/4/8 query heads per kv head): prefill, a few appended
+    tokens, decode at the last position vs the oracle's single-row restatement."""
+    import random
+
+    import torch
+
+    rng = random.Random(9000 + seed)
+    Hkv = rng.choice([1, 2, 4])
+    hpg = rng.choice([1, 2, 4, 8])
+    H = Hkv * hpg
+    D = rng.choice([64, 128])
+    blocks = rng.randint(2, 48)
+    N = blocks * 64 - rng.randrange(64)
+    batch = rng.randint(1, 3)
+    local = 1 + rng.randrange(min(4, blocks))
+    vs = rng.randint(1, 8)
+    cfg = single(N, 64, H, local, vs, kv=Hkv)
+    plan = s2.Plan.from_config(cfg)
+    cache = KVCache(plan, batch, D)
+    T0 = rng.randint(1, N - 1)
+    T = min(N, T0 + rng.randint(0, 5))
+    k, vv = _dense(batch, Hkv, T, D, seed)
+    dev = torch.device("cuda")
+    tk = torch.from_numpy(k).reshape(batch, Hkv, T, D).to(dev, torch.bfloat16)
+    tv = torch.from_numpy(vv).reshape(batch, Hkv, T, D).to(dev, torch.bfloat16)
+    cache.prefill(tk[:, :, :T0].contiguous(), tv[:, :, :T0].contiguous())
+    for t in range(T0, T):
+        cache.append(tk[:, :, t].contiguous(), tv[:, :, t].contiguous())
+    assert cache.length == T
+    q = bf16_round(np.random.default_rng(seed).uniform(-1, 1, batch * H * D).astype(np.float32))
+    out, lse = cache.decode(torch.from_numpy(q).reshape(batch, H, D).to(dev, torch.bfloat16))
+    torch.cuda.synchronize()
+    rp, ci = oracle.csr_all(cfg)
+    ro, rl = oracle.decode(q, k, vv, rp, ci, batch, H, Hkv, T, D, 64, T - 1, cfg.num_blocks())
+    np.testing.assert_allclose(out.float().cpu().numpy().ravel(), ro, rtol=1e-2, atol=1e-2)
+    np.testing.assert_allclose(lse.cpu().numpy().ravel(), rl, rtol=1e-3, atol=1e-3)
