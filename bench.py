@@ -317,7 +317,6 @@ def run_s2(args):
         step()
     barrier()
     lib = _abi.lib()
-    lib.s2_profile_enable(1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -327,6 +326,13 @@ def run_s2(args):
         e1.record()
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    # per-kernel breakdown: the same steps again with CUDA events around every
+    # launch (kept out of the timed loop: events between launches would serialise
+    # its programmatic dependent launches)
+    lib.s2_profile_enable(1)
+    for _ in range(args.steps):
+        step()
+    barrier()
     names = ctypes.create_string_buffer(32 * 16)
     tot = (ctypes.c_double * 16)()
     cnt = (ctypes.c_int * 16)()

@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(256) s2_bwd_prep_kernel(const __nv_bfloat16* _
                                                           int N, int Npad) {
     // Rows in 32-bit arithmetic (the host checks num_bh * Npad < 2^31): a 64-bit
     // divide / modulo per row made this kernel issue-bound, not HBM-bound.
+    pdl_launch_dependents();
+    pdl_wait();
     constexpr int LPR = D / 8;  // lanes per row
     constexpr int kRows = S2_PREP_ROWS;  // rows per thread per sweep (2 x kRows 16-byte loads in flight)
     const uint32_t total = static_cast<uint32_t>(num_bh) * static_cast<uint32_t>(Npad);
@@ -218,6 +220,8 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
+    pdl_launch_dependents();
+    pdl_wait();  // the previous kernel's outputs are visible from here on
     if (p.trace && tid == 0) p.trace[15 * 2048 + 2 * blockIdx.x] = globaltimer_ns();  // debug: CTA start
     // TMEM: V at 0 (the dP^T A operand: copied in once per item with tcgen05.cp, so
     // the per-step dP^T MMAs read only the 2 KB dO slices from shared memory),
@@ -611,6 +615,8 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
+    pdl_launch_dependents();
+    pdl_wait();  // the previous kernel's outputs are visible from here on
     if (p.trace && tid == 0) p.trace[15 * 2048 + 2 * blockIdx.x] = globaltimer_ns();  // debug: CTA start
     // TMEM: Q at 0 and dO at 64 (the S / dP A operands, copied in with tcgen05.cp once
     // per item: the per-step MMAs then read only the 2 KB K / V slices from shared
@@ -848,9 +854,11 @@ cudaError_t s2_launch_bwd_prep(const __nv_bfloat16* out, const __nv_bfloat16* do
     const long long need = (rows + per_block - 1) / per_block;
     const int blocks = static_cast<int>(std::min<long long>(need, 148LL * 8));
     if (D == 128)
-        s2_bwd_prep_kernel<128><<<blocks, 256, 0, stream>>>(out, dout, lse, delta, lse2, num_bh, N, Npad);
+        return launch_pdl(s2_bwd_prep_kernel<128>, dim3(blocks), dim3(256), 0, stream, out, dout, lse, delta, lse2,
+                          num_bh, N, Npad);
     else if (D == 64)
-        s2_bwd_prep_kernel<64><<<blocks, 256, 0, stream>>>(out, dout, lse, delta, lse2, num_bh, N, Npad);
+        return launch_pdl(s2_bwd_prep_kernel<64>, dim3(blocks), dim3(256), 0, stream, out, dout, lse, delta, lse2,
+                          num_bh, N, Npad);
     else
         return cudaErrorInvalidValue;
     return cudaGetLastError();
@@ -863,8 +871,7 @@ static cudaError_t launch_bwd(K kern, int smem, int grid, const CUtensorMap& q,
                               cudaStream_t stream) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 384, smem, stream>>>(q, dout, k, v, o0, o1, p);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(grid), dim3(384), smem, stream, q, dout, k, v, o0, o1, p);
 }
 
 // which = 0: dK/dV kernel (q/do: 64-row boxes; o0 = dK, o1 = dV maps with 64-row

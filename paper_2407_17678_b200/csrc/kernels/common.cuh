@@ -45,3 +45,34 @@ struct DecodeParams {
 };
 
 }  // namespace s2dev
+
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+namespace s2dev {
+// Launch with programmatic stream serialization (PDL) unless S2_PDL=0: the
+// kernels call griddepcontrol.launch_dependents / .wait, so the next kernel's
+// CTAs are scheduled as this one's exit and do their setup during its tail.
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("S2_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+template <typename Kern, typename... Args>
+inline cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+}  // namespace s2dev

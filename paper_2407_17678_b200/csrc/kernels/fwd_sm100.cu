@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
+    pdl_launch_dependents();
+    pdl_wait();  // the previous kernel's outputs are visible from here on
     if (p.trace && tid == 0) p.trace[15 * 2048 + 2 * blockIdx.x] = globaltimer_ns();  // debug: CTA start
 
     if (warp < 4) {
@@ -555,15 +557,13 @@ static cudaError_t launch(const CUtensorMap& q, const CUtensorMap& k, const CUte
         cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::kSmem);
         if (e != cudaSuccess) return e;
-        kern<<<grid, 384, Fwd2Cfg<D>::kSmem, stream>>>(q, k, v, o, p, NoPeers{});
-        return cudaGetLastError();
+        return launch_pdl(kern, dim3(grid), dim3(384), Fwd2Cfg<D>::kSmem, stream, q, k, v, o, p, NoPeers{});
     }
     auto kern = s2_fwd_sm100_kernel<D, true>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::kSmem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 384, Fwd2Cfg<D>::kSmem, stream>>>(q, k, v, o, p, px);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(grid), dim3(384), Fwd2Cfg<D>::kSmem, stream, q, k, v, o, p, px);
 }
 
 }  // namespace s2dev

@@ -341,4 +341,13 @@ __device__ __forceinline__ long long globaltimer_ns() {
     return t;
 }
 
+// Programmatic dependent launch (PDL): let the next kernel in the stream be
+// scheduled now (its CTAs take SMs as ours exit and run their local setup),
+// and wait for the previous kernel's completion (+ memory visibility) before
+// touching global memory.  No-ops without the launch attribute.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace s2dev
