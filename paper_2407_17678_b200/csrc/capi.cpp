@@ -176,6 +176,13 @@ static int dkv_group() {
     return e ? atoi(e) : 0;
 }
 
+// per-item overhead of the LPT cost model, in step units (tuning knob: env
+// S2_SCHED_OVH_<kind>)
+static int64_t sched_overhead(const char* env, int64_t dflt) {
+    const char* e = getenv(env);
+    return e ? atoll(e) : dflt;
+}
+
 // Units are (batch, kv-group); local data index of query head j of the
 // ui-th listed unit is ui*hpg + j (= b*H + h when every unit is listed).
 WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* unit_ids,
@@ -226,7 +233,7 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
             }
         const std::vector<int32_t> off_fwd = schedule_items(
             fi, grid, [](const s2dev::FwdItem& a) { return int64_t(a.chunk_cnt); },
-            [](const s2dev::FwdItem& a) { return a.bh; }, 2);
+            [](const s2dev::FwdItem& a) { return a.bh; }, sched_overhead("S2_SCHED_OVH_DQ", 2));
         struct PairItem {
             int32_t bh, qpair, nsteps, has_b;
             int64_t step_off;
@@ -242,7 +249,7 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
             }
         const std::vector<int32_t> off_pair = schedule_items(
             pi, grid, [](const PairItem& a) { return int64_t(a.nsteps) * (1 + a.has_b); },
-            [](const PairItem& a) { return a.bh; }, 4);
+            [](const PairItem& a) { return a.bh; }, sched_overhead("S2_SCHED_OVH_FWD", 4));
         w->num_pair = static_cast<int>(pi.size());
         if ((e = upload(w->pair, pi.data(), pi.size() * sizeof(PairItem))) != cudaSuccess ||
             (e = upload(w->pair_sched, off_pair.data(), off_pair.size() * sizeof(int32_t))) != cudaSuccess ||
@@ -275,7 +282,8 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
         w->bwd_dropped = bi.size() != nb_all;
         auto bwd_cost = [](const s2dev::BwdItem& a) { return int64_t(a.nsteps); };
         const std::vector<int32_t> off_bwd = schedule_items(
-            bi, grid, bwd_cost, [](const s2dev::BwdItem& a) { return a.kvbh; }, 4, dkv_group());
+            bi, grid, bwd_cost, [](const s2dev::BwdItem& a) { return a.kvbh; }, sched_overhead("S2_SCHED_OVH_DKV", 4),
+            dkv_group());
         w->num_fwd = static_cast<int>(fi.size());
         w->num_bwd = static_cast<int>(bi.size());
         w->grid = grid;
