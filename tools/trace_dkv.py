@@ -61,3 +61,17 @@ ni2 = int((t[14] != -t0).sum())
 if ni2 > 3:
     e = t[:, 1:ni2 - 1].astype(np.float64)
     print(f"dq items traced {ni2}: MMA wait for the next item's Q/dO (bar_qf) median {np.median(e[14] - e[13]):.0f} cycles")
+    # where the dQ kernel's time goes: steady steps vs item boundaries
+    sc = t[2, :n].astype(np.float64)
+    starts = t[14, 1:ni2].astype(np.float64)  # issuer has the next item's Q/dO
+    first = np.searchsorted(sc, starts)       # index of the first S commit of each item
+    first = first[(first > 0) & (first < n)]
+    st = np.diff(sc)
+    med = np.median(st)
+    bd = sc[first] - sc[first - 1]
+    print(f"dq: {n} steps, median step {med:.0f} cyc, total {sc[-1] - sc[0]:.0f}; "
+          f"{len(first)} item boundaries: median gap {np.median(bd):.0f} cyc, "
+          f"boundary excess {np.sum(bd - med) / (sc[-1] - sc[0]):.1%} of the time; "
+          f"non-boundary steps > 1.5x median carry {np.sum(st[st > 1.5 * med]) / st.sum():.1%}")
+    print("EW compute median", np.median(t[7, :n] - t[6, :n]), " EW wait S median", np.median(t[6, :n] - t[5, :n]),
+          " MMA wait P median", np.median(t[4, :n - 1] - t[3, :n - 1]))
