@@ -76,6 +76,23 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def use_all_host_threads():
+    """The CPU legs run on every host core. torchrun exports OMP_NUM_THREADS=1, so the
+    variable is overridden (not defaulted), and the thread count is set directly on
+    the libgomp that oracle/ links, in case it has already read its environment.
+    Returns the thread count in effect, which is what `cores` reports."""
+    import ctypes
+
+    n = host_cores()
+    os.environ["OMP_NUM_THREADS"] = str(n)
+    try:
+        gomp = ctypes.CDLL("libgomp.so.1")
+        gomp.omp_set_num_threads(ctypes.c_int(n))
+        return int(gomp.omp_get_max_threads())
+    except OSError:
+        return n
+
+
 # ---------------------------------------------------------------- CPU side
 def cpu_sample(heads=(0,), seed=7, band=1.0):
     """Time the reference CPU path on a bounded sample: fwd through the
@@ -84,6 +101,7 @@ def cpu_sample(heads=(0,), seed=7, band=1.0):
     (the other rows' CSR lists are emptied; rows in the middle of the sequence
     have the average row length), bounding the work per step.
     Returns (tflops, seconds, kind, sample_desc, flops)."""
+    threads = use_all_host_threads()
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle  # test/baseline infrastructure only
 
@@ -119,14 +137,15 @@ def cpu_sample(heads=(0,), seed=7, band=1.0):
             assert rc == 0
         else:
             oracle.attn_fwd(q, k, v, rp, ci, 1, 1, 1, N_SEQ, D, BLOCK)
-        oracle.attn_bwd(q, k, v, do, rp, ci, 1, 1, 1, N_SEQ, D, BLOCK)
+        oracle.attn_bwd_par(q, k, v, do, rp, ci, 1, 1, 1, N_SEQ, D, BLOCK)
         tot_s += time.perf_counter() - t0
         flops += 3.5 * int(ci.size) * 4.0 * D * BLOCK * BLOCK
     desc = (f"cfg3 heads {list(heads)} of {H}" + (f", centred band of {band:g} of the query blocks" if band < 1 else "")
             + " (fwd: "
             f"{'reference streaming_sharded_attention' if kind == 'reference' else 'oracle port'}"
-            f"; bwd: oracle C restatement, the reference has no backward), fp32/fp64, "
-            f"{host_cores()} threads")
+            f"; bwd: oracle C restatement parallel over rows and key blocks, the reference has "
+            "no backward), fp32/fp64, "
+            f"{threads} threads")
     return flops / tot_s / 1e12, tot_s, kind, desc, flops
 
 
@@ -134,14 +153,14 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
-    # bounded steps: a 1/8 band of one head per step (~2 s on 16 cores), warm-up 1/64
+    use_all_host_threads()
+    # bounded steps: a 1/2 band of one head per step (~1-2 s on 16 cores), warm-up 1/16
     for _ in range(args.warmup):
-        cpu_sample(heads=(0,), band=1.0 / 64)
+        cpu_sample(heads=(0,), band=1.0 / 16)
     vals, secs = [], []
     kind = desc = None
     for i in range(args.steps):
-        v, s, kind, desc, _ = cpu_sample(heads=(i % H,), band=1.0 / 8)
+        v, s, kind, desc, _ = cpu_sample(heads=(i % H,), band=1.0 / 2)
         vals.append(v)
         secs.append(s)
     value = float(np.mean(vals))
@@ -151,7 +170,7 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": 1000 * float(np.mean(secs)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config_desc(args.gpus),
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": host_cores(), "kind": kind,
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": use_all_host_threads(), "kind": kind,
                          "sample": desc + "; one head band per step"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -452,9 +471,9 @@ def run_s2(args):
     # ---- CPU baseline (rank 0, N=1 only)
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
-            os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
-            val, secs, kind, desc, fl = cpu_sample(heads=(0,))
-            line["cpu_baseline"] = {"value": val, "unit": "TFLOP/s", "cores": host_cores(),
+            threads = use_all_host_threads()
+            val, secs, kind, desc, fl = cpu_sample(heads=(0, 1, 2, 3))
+            line["cpu_baseline"] = {"value": val, "unit": "TFLOP/s", "cores": threads,
                                     "kind": kind, "sample": desc, "seconds": secs}
         except Exception as ex:  # reported, never fatal to the GPU number
             line["cpu_baseline"] = {"value": None, "error": str(ex)}

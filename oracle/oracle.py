@@ -72,6 +72,8 @@ def port():
                                                          _F, _D]),
             "s2o_attn_bwd": (None, [ctypes.c_int] * 6 + [ctypes.c_double, _F, _F, _F, _F, _IP,
                                                          _IP, _F, _F, _F]),
+            "s2o_attn_bwd_par": (None, [ctypes.c_int] * 6 + [ctypes.c_double, _F, _F, _F, _F, _IP,
+                                                         _IP, _F, _F, _F]),
             "s2o_decode": (None, [ctypes.c_int] * 7 + [ctypes.c_double, _F, _F, _F,
                                                        _IP, _IP, ctypes.c_int, _F, _D]),
             "s2o_bwd_sample": (None, [ctypes.c_int] * 6 + [ctypes.c_double, _F, _F, _F, _F, _IP, _IP,
@@ -194,6 +196,20 @@ def attn_bwd(q, k, v, dout, row_ptr, col_idx, batch, H, Hkv, N, D, S, scale=None
     port().s2o_attn_bwd(batch, H, Hkv, N, D, S, scale, fp(q), fp(k), fp(v), fp(dout),
                         ip(np.ascontiguousarray(row_ptr, np.int32)),
                         ip(np.ascontiguousarray(col_idx, np.int32)), fp(dq), fp(dk), fp(dv))
+    return dq, dk, dv
+
+
+def attn_bwd_par(q, k, v, dout, row_ptr, col_idx, batch, H, Hkv, N, D, S, scale=None):
+    """attn_bwd parallel inside a unit (s2o_attn_bwd_par): the same values, bit for
+    bit; bench.py's CPU-baseline legs use it so that one head uses every core."""
+    scale = 1.0 / np.sqrt(D) if scale is None else scale
+    q, k, v, dout = (np.ascontiguousarray(x, np.float32) for x in (q, k, v, dout))
+    dq = np.zeros_like(q)
+    dk = np.zeros_like(k)
+    dv = np.zeros_like(v)
+    port().s2o_attn_bwd_par(batch, H, Hkv, N, D, S, scale, fp(q), fp(k), fp(v), fp(dout),
+                            ip(np.ascontiguousarray(row_ptr, np.int32)),
+                            ip(np.ascontiguousarray(col_idx, np.int32)), fp(dq), fp(dk), fp(dv))
     return dq, dk, dv
 
 

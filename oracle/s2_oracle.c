@@ -420,6 +420,165 @@ void s2o_attn_bwd(int batch, int H, int Hkv, int N, int D, int S, double scale, 
     free(col_off);
 }
 
+/* s2o_attn_bwd, parallel inside a (batch, kv-group) unit: bit-identical results,
+ * for the CPU baseline legs of bench.py (one unit is a single thread's work in
+ * s2o_attn_bwd).  Pass 1, parallel over query rows: each row's max, sum, delta
+ * and dQ, computed exactly as s2o_attn_bwd does.  Pass 2, parallel over key
+ * blocks: dK / dV of each key summed over (query head of the group, attending
+ * row) in ascending order -- s2o_attn_bwd's accumulation order -- with p and dp
+ * recomputed from the same expressions.  Test infrastructure only. */
+void s2o_attn_bwd_par(int batch, int H, int Hkv, int N, int D, int S, double scale, const float* q,
+                      const float* k, const float* v, const float* dout, const int* row_ptr,
+                      const int* col_idx, float* dq, float* dk, float* dv) {
+    const int B = (N + S - 1) / S;
+    const int hpg = H / Hkv;
+    int64_t* col_off = (int64_t*)malloc(sizeof(int64_t) * (size_t)H);
+    head_offsets(H, B, row_ptr, col_off);
+    double* mrow = (double*)malloc(sizeof(double) * (size_t)N * hpg);
+    double* zrow = (double*)malloc(sizeof(double) * (size_t)N * hpg);
+    double* drow = (double*)malloc(sizeof(double) * (size_t)N * hpg);
+    /* per head of a group: for each key block, the row blocks listing it (ascending) */
+    int* cptr = (int*)malloc(sizeof(int) * (size_t)(B + 1) * hpg);
+    int* crow = NULL;
+    for (int u = 0; u < batch * Hkv; ++u) {
+        const int b = u / Hkv, g = u % Hkv;
+        const float* K = k + (size_t)u * N * D;
+        const float* V = v + (size_t)u * N * D;
+        int64_t nnz_g = 0;
+        for (int hh = 0; hh < hpg; ++hh) {
+            const int* rp = row_ptr + (size_t)(g * hpg + hh) * (B + 1);
+            nnz_g += rp[B];
+        }
+        crow = (int*)realloc(crow, sizeof(int) * (size_t)(nnz_g > 0 ? nnz_g : 1));
+        int64_t base = 0;
+        for (int hh = 0; hh < hpg; ++hh) {
+            const int h = g * hpg + hh;
+            const int* rp = row_ptr + (size_t)h * (B + 1);
+            const int* ci = col_idx + col_off[h];
+            int* cp = cptr + (size_t)hh * (B + 1);
+            for (int c = 0; c <= B; ++c) cp[c] = 0;
+            for (int e = 0; e < rp[B]; ++e) cp[ci[e] + 1]++;
+            for (int c = 0; c < B; ++c) cp[c + 1] += cp[c];
+            int* fill = (int*)malloc(sizeof(int) * (size_t)B);
+            for (int c = 0; c < B; ++c) fill[c] = cp[c];
+            for (int bi = 0; bi < B; ++bi)  /* ascending rows per column */
+                for (int e = rp[bi]; e < rp[bi + 1]; ++e) crow[base + fill[ci[e]]++] = bi;
+            free(fill);
+            for (int c = 0; c <= B; ++c) cp[c] += (int)base;
+            base += rp[B];
+        }
+        /* pass 1: rows */
+        for (int hh = 0; hh < hpg; ++hh) {
+            const int h = g * hpg + hh;
+            const size_t qo = ((size_t)b * H + h) * N * D;
+            const int* rp = row_ptr + (size_t)h * (B + 1);
+            const int* ci = col_idx + col_off[h];
+#pragma omp parallel
+            {
+                double* sc = (double*)malloc(sizeof(double) * (size_t)N);
+                double* o = (double*)malloc(sizeof(double) * (size_t)D);
+                double* gq = (double*)malloc(sizeof(double) * (size_t)D);
+#pragma omp for schedule(dynamic, 16)
+                for (int i = 0; i < N; ++i) {
+                    const int bi = i / S;
+                    const float* qi = q + qo + (size_t)i * D;
+                    const float* doi = dout + qo + (size_t)i * D;
+                    double mx = -INFINITY;
+                    for (int ptr = rp[bi]; ptr < rp[bi + 1]; ++ptr) {
+                        const int j0 = ci[ptr] * S;
+                        for (int j = j0; j < j0 + S && j <= i; ++j) {
+                            double dot = 0.0;
+                            for (int x = 0; x < D; ++x) dot += (double)qi[x] * K[(size_t)j * D + x];
+                            sc[j] = scale * dot;
+                            if (sc[j] > mx) mx = sc[j];
+                        }
+                    }
+                    double z = 0.0;
+                    for (int x = 0; x < D; ++x) o[x] = 0.0;
+                    for (int ptr = rp[bi]; ptr < rp[bi + 1]; ++ptr) {
+                        const int j0 = ci[ptr] * S;
+                        for (int j = j0; j < j0 + S && j <= i; ++j) {
+                            sc[j] = exp(sc[j] - mx);
+                            z += sc[j];
+                            for (int x = 0; x < D; ++x) o[x] += sc[j] * V[(size_t)j * D + x];
+                        }
+                    }
+                    double delta = 0.0;
+                    for (int x = 0; x < D; ++x) {
+                        o[x] /= z;
+                        delta += (double)doi[x] * o[x];
+                    }
+                    for (int x = 0; x < D; ++x) gq[x] = 0.0;
+                    for (int ptr = rp[bi]; ptr < rp[bi + 1]; ++ptr) {
+                        const int j0 = ci[ptr] * S;
+                        for (int j = j0; j < j0 + S && j <= i; ++j) {
+                            const double pij = sc[j] / z;
+                            double dp = 0.0;
+                            for (int x = 0; x < D; ++x) dp += (double)doi[x] * V[(size_t)j * D + x];
+                            const double ds = pij * (dp - delta);
+                            for (int x = 0; x < D; ++x) gq[x] += ds * K[(size_t)j * D + x];
+                        }
+                    }
+                    for (int x = 0; x < D; ++x) dq[qo + (size_t)i * D + x] = (float)(scale * gq[x]);
+                    mrow[(size_t)hh * N + i] = mx;
+                    zrow[(size_t)hh * N + i] = z;
+                    drow[(size_t)hh * N + i] = delta;
+                }
+                free(sc);
+                free(o);
+                free(gq);
+            }
+        }
+        /* pass 2: key blocks */
+#pragma omp parallel
+        {
+            double* gk = (double*)malloc(sizeof(double) * (size_t)D);
+            double* gv = (double*)malloc(sizeof(double) * (size_t)D);
+#pragma omp for schedule(dynamic)
+            for (int cb = 0; cb < B; ++cb) {
+                for (int j = cb * S; j < cb * S + S && j < N; ++j) {
+                    for (int x = 0; x < D; ++x) gk[x] = gv[x] = 0.0;
+                    for (int hh = 0; hh < hpg; ++hh) {
+                        const int h = g * hpg + hh;
+                        const size_t qo = ((size_t)b * H + h) * N * D;
+                        const int* cp = cptr + (size_t)hh * (B + 1);
+                        for (int e = cp[cb]; e < cp[cb + 1]; ++e) {
+                            const int bi = crow[e];
+                            for (int i = bi * S; i < bi * S + S && i < N; ++i) {
+                                if (j > i) continue;
+                                const float* qi = q + qo + (size_t)i * D;
+                                const float* doi = dout + qo + (size_t)i * D;
+                                double dot = 0.0;
+                                for (int x = 0; x < D; ++x) dot += (double)qi[x] * K[(size_t)j * D + x];
+                                const double pij = exp(scale * dot - mrow[(size_t)hh * N + i]) / zrow[(size_t)hh * N + i];
+                                double dp = 0.0;
+                                for (int x = 0; x < D; ++x) dp += (double)doi[x] * V[(size_t)j * D + x];
+                                const double ds = pij * (dp - drow[(size_t)hh * N + i]);
+                                for (int x = 0; x < D; ++x) {
+                                    gk[x] += ds * qi[x];
+                                    gv[x] += pij * doi[x];
+                                }
+                            }
+                        }
+                    }
+                    for (int x = 0; x < D; ++x) {
+                        dk[(size_t)u * N * D + (size_t)j * D + x] = (float)(scale * gk[x]);
+                        dv[(size_t)u * N * D + (size_t)j * D + x] = (float)gv[x];
+                    }
+                }
+            }
+            free(gk);
+            free(gv);
+        }
+    }
+    free(crow);
+    free(cptr);
+    free(mrow);
+    free(zrow);
+    free(drow);
+    free(col_off);
+}
+
 /* ------------------------------------------------- sampled backward rows */
 
 /* Row statistics of query row i (reference.cpp:28-45 two-pass): max m, sum z

@@ -228,3 +228,32 @@ def test_port_sampled_backward_rows_equal_full_backward(case):
     for n, (g, j) in enumerate(k_rows):
         np.testing.assert_allclose(sk[n], dk[g, j], rtol=1e-5, atol=1e-6)
         np.testing.assert_allclose(sv[n], dv[g, j], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("case", ["gqa_ragged", "batch2", "local_stride"])
+def test_parallel_port_backward_is_bit_identical(case):
+    """s2o_attn_bwd_par (the CPU baseline's backward: parallel over rows, then over
+    key blocks) equals s2o_attn_bwd bit for bit -- same expressions, same dK / dV
+    accumulation order -- at any thread count."""
+    import ctypes
+
+    if case == "gqa_ragged":
+        cfg, batch, D = single(300, 16, 4, 2, 3, kv=2), 1, 32
+    elif case == "batch2":
+        cfg, batch, D = single(256, 32, 2, 1, 2), 2, 16
+    else:
+        cfg, batch, D = single(500, 32, 4, 3, 2), 1, 16
+        cfg.local_stride = 2
+        cfg.validate()
+    H, Hkv, N, S = cfg.num_heads, cfg.kv_heads(), cfg.seq_len, cfg.block_size
+    rng = np.random.default_rng(12)
+    q, do = (rng.uniform(-1, 1, batch * H * N * D).astype(np.float32) for _ in range(2))
+    k, v = (rng.uniform(-1, 1, batch * Hkv * N * D).astype(np.float32) for _ in range(2))
+    rp, ci = oracle.csr_all(cfg)
+    ref = oracle.attn_bwd(q, k, v, do, rp, ci, batch, H, Hkv, N, D, S)
+    gomp = ctypes.CDLL("libgomp.so.1")
+    for threads in (1, 3, 8):
+        gomp.omp_set_num_threads(threads)
+        par = oracle.attn_bwd_par(q, k, v, do, rp, ci, batch, H, Hkv, N, D, S)
+        for a, b in zip(par, ref):
+            np.testing.assert_array_equal(a, b)
