@@ -472,7 +472,7 @@ def run_s2(args):
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
             threads = use_all_host_threads()
-            val, secs, kind, desc, fl = cpu_sample(heads=(0, 1, 2, 3))
+            val, secs, kind, desc, fl = cpu_sample(heads=tuple(range(8)))
             line["cpu_baseline"] = {"value": val, "unit": "TFLOP/s", "cores": threads,
                                     "kind": kind, "sample": desc, "seconds": secs}
         except Exception as ex:  # reported, never fatal to the GPU number
