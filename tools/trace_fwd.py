@@ -15,12 +15,12 @@ plan = s2.Plan.from_config(s2.make_s2_config(32768, 32, local_blocks=4, vert_str
 mk = lambda: torch.randn(1, 32, 32768, 128, device="cuda", dtype=torch.bfloat16)  # noqa
 q, k, v = mk(), mk(), mk()
 out, lse = s2.s2_attn_fwd(plan, q, k, v)
-tr = torch.zeros(16 * 2048, dtype=torch.int64, device="cuda")
+tr = torch.zeros(24 * 2048, dtype=torch.int64, device="cuda")
 L.s2_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
 s2.s2_attn_fwd(plan, q, k, v, out=out, lse=lse)
 torch.cuda.synchronize()
 L.s2_debug_set_trace(None)
-t = tr.cpu().numpy().reshape(16, 2048).astype(np.int64)
+t = tr.cpu().numpy().reshape(24, 2048).astype(np.int64)
 n = int((t[5] > 0).sum())
 m = lambda a: float(np.median(a))  # noqa
 lo, hi = 20, min(n, 1500)
@@ -59,3 +59,7 @@ if (t[12] > 0).sum() > 10:  # built with -DS2_FWD_DETAIL_TRACE
         cur = t[8 + i, k]
         print(f"  {nm}: {np.median(cur - prev):.0f}")
         prev = cur
+
+if (t[16] > 0).sum() > 40:
+    print(f"softmax0 gap split: P arrive -> next chunk's loop top {m(t[16, lo + 1:hi + 1] - t[8, lo:hi]):.0f}, "
+          f"loop top -> wait {m(t[4, lo + 1:hi + 1] - t[16, lo + 1:hi + 1]):.0f}")
