@@ -237,3 +237,20 @@ def test_f32_negative_control_corrupted_csr_fails_parity():
     s2.streaming_sharded_attention(t2, s2.build_all_csr(cfg), p["S"])
     out2 = t2.out[FWD_ARR[name + "__out_idx"]] if name + "__out_idx" in FWD_ARR else t2.out
     np.testing.assert_allclose(out2, FWD_ARR[name + "__out"], **F32_TOL)
+
+
+@pytest.mark.parametrize("d", [3, 24, 40, 96, 200, 256])
+def test_f32_any_head_dim_matches_oracle(d):
+    """The reference takes any head dim (AttentionTensors d, attention.hpp:17-37); the
+    fp32 kernel serves every d <= 256.  Unusual sizes vs the oracle port (itself
+    bit-identical to the reference's streaming forward), at the fp32 tolerance."""
+    cfg = s2.make_single_stride_config(300, 16, 3, 2, 3)
+    H, N = 3, 300
+    q, k, v = oracle.random_tensors(H, N, d, 40 + d)
+    t = s2.AttentionTensors.zeros(H, N, d)
+    t.q, t.k, t.v = q, k, v
+    s2.streaming_sharded_attention(t, s2.build_all_csr(cfg), 16)
+    rp, ci = oracle.csr_all(cfg)
+    ro, rl = oracle.attn_fwd(q, k, v, rp, ci, 1, H, H, N, d, 16)
+    np.testing.assert_allclose(t.out, ro, **F32_TOL)
+    np.testing.assert_allclose(t.lse, rl, **F32_TOL)
