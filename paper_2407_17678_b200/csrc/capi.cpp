@@ -701,8 +701,8 @@ static int attn_fwd_impl(s2_plan* p, const s2_attn_args* a, int num_peers, void*
             return fail(S2_ERR_CUDA, ex.what());
         }
     } else {
-        if (a->head_dim > 256)
-            return fail(S2_ERR_UNSUPPORTED, "head_dim > 256 is not supported");
+        if (a->head_dim > 2048)
+            return fail(S2_ERR_UNSUPPORTED, "head_dim > 2048 is not supported");
         if ((rc = ensure_csr_uploaded(p))) return rc;
         ProfScope prof("fwd_simt", st);
         e = s2_launch_fwd_simt(a->dtype == S2_DTYPE_BF16, a->q, a->k, a->v, a->out, a->lse,

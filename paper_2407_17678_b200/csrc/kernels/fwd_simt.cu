@@ -11,6 +11,8 @@
 // reference's exactness tests (test_attention.cpp:196-257).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <type_traits>
 #include <stdint.h>
 
 namespace s2dev {
@@ -38,9 +40,10 @@ struct SimtParams {
     float scale;
 };
 
-constexpr int kMaxDPerLane = 8;  // head_dim <= 256
+// head_dim <= 32 * DPL: instantiated for DPL 8 / 16 / 64 (head_dim <= 256 / 512 / 2048)
+constexpr int kMaxHeadDim = 2048;
 
-template <typename T>
+template <typename T, int DPL>
 __global__ void __launch_bounds__(128) s2_fwd_simt_kernel(const T* __restrict__ q,
                                                           const T* __restrict__ k,
                                                           const T* __restrict__ v,
@@ -69,9 +72,9 @@ __global__ void __launch_bounds__(128) s2_fwd_simt_kernel(const T* __restrict__ 
         for (int x = lane; x < D; x += 32) qs[x] = to_f(Q[static_cast<size_t>(i) * D + x]);
         __syncwarp();
         float m = -INFINITY, l = 0.f;
-        float acc[kMaxDPerLane];
+        float acc[DPL];
 #pragma unroll
-        for (int e = 0; e < kMaxDPerLane; ++e) acc[e] = 0.f;
+        for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
         for (int ptr = rp[qb]; ptr < rp[qb + 1]; ++ptr) {
             const int k_begin = ci[ptr] * S;
             const int k_end = min(min(k_begin + S, N), i + 1);
@@ -95,13 +98,13 @@ __global__ void __launch_bounds__(128) s2_fwd_simt_kernel(const T* __restrict__ 
                 for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
                 l = l * alpha + ps;
 #pragma unroll
-                for (int e = 0; e < kMaxDPerLane; ++e) acc[e] *= alpha;
+                for (int e = 0; e < DPL; ++e) acc[e] *= alpha;
                 const int nk = min(32, k_end - kc);
                 for (int kk = 0; kk < nk; ++kk) {
                     const float w = __shfl_sync(0xffffffffu, pv, kk);
                     const T* vr = V + static_cast<size_t>(kc + kk) * D;
 #pragma unroll
-                    for (int e = 0; e < kMaxDPerLane; ++e) {
+                    for (int e = 0; e < DPL; ++e) {
                         const int x = lane + 32 * e;
                         if (e < nd && x < D) acc[e] = fmaf(w, to_f(vr[x]), acc[e]);
                     }
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(128) s2_fwd_simt_kernel(const T* __restrict__ 
         }
         const float inv = 1.0f / l;
 #pragma unroll
-        for (int e = 0; e < kMaxDPerLane; ++e) {
+        for (int e = 0; e < DPL; ++e) {
             const int x = lane + 32 * e;
             if (e < nd && x < D) out[static_cast<size_t>(bh) * N * D + static_cast<size_t>(i) * D + x] = from_f<T>(acc[e] * inv);
         }
@@ -128,17 +131,26 @@ cudaError_t s2_launch_fwd_simt(bool bf16, const void* q, const void* k, const vo
                                int N, int D, int S, int B, int hpg, float scale,
                                cudaStream_t stream) {
     if (num_bh == 0) return cudaSuccess;
-    if (D > 32 * s2dev::kMaxDPerLane) return cudaErrorInvalidValue;
+    if (D > s2dev::kMaxHeadDim) return cudaErrorInvalidValue;
     s2dev::SimtParams p{bh_list, head_of, row_ptr, col_idx, col_off, num_bh, N, D, S, B, hpg, scale};
     dim3 grid(B, num_bh);
-    const size_t smem = 4 * D * sizeof(float);
-    if (bf16)
-        s2dev::s2_fwd_simt_kernel<__nv_bfloat16><<<grid, 128, smem, stream>>>(
-            static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
-            static_cast<const __nv_bfloat16*>(v), static_cast<__nv_bfloat16*>(out), lse, p);
+    const size_t smem = 4 * D * sizeof(float);  // <= 32 KB
+    auto launch = [&](auto tag) {
+        constexpr int DPL = decltype(tag)::value;
+        if (bf16)
+            s2dev::s2_fwd_simt_kernel<__nv_bfloat16, DPL><<<grid, 128, smem, stream>>>(
+                static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
+                static_cast<const __nv_bfloat16*>(v), static_cast<__nv_bfloat16*>(out), lse, p);
+        else
+            s2dev::s2_fwd_simt_kernel<float, DPL><<<grid, 128, smem, stream>>>(
+                static_cast<const float*>(q), static_cast<const float*>(k), static_cast<const float*>(v),
+                static_cast<float*>(out), lse, p);
+    };
+    if (D <= 256)
+        launch(std::integral_constant<int, 8>{});
+    else if (D <= 512)
+        launch(std::integral_constant<int, 16>{});
     else
-        s2dev::s2_fwd_simt_kernel<float><<<grid, 128, smem, stream>>>(
-            static_cast<const float*>(q), static_cast<const float*>(k), static_cast<const float*>(v),
-            static_cast<float*>(out), lse, p);
+        launch(std::integral_constant<int, 64>{});
     return cudaGetLastError();
 }
