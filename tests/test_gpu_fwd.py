@@ -254,3 +254,23 @@ def test_f32_any_head_dim_matches_oracle(d):
     ro, rl = oracle.attn_fwd(q, k, v, rp, ci, 1, H, H, N, d, 16)
     np.testing.assert_allclose(t.out, ro, **F32_TOL)
     np.testing.assert_allclose(t.lse, rl, **F32_TOL)
+
+
+@pytest.mark.parametrize("d", [32, 96, 256])
+def test_bf16_other_head_dims_take_the_simt_kernel_and_match_oracle(d):
+    """bf16 with a head dim the tensor-core kernel does not take (not 64 / 128) runs
+    the SIMT kernel on bf16 data: parity with the oracle at the bf16 tolerance."""
+    import torch
+
+    cfg = single(700, 64, 4, 2, 3, kv=2)
+    H, Hkv, N, S = 4, 2, 700, 64
+    rng = np.random.default_rng(d)
+    q = bf16_round(rng.uniform(-1, 1, H * N * d).astype(np.float32))
+    k, v = (bf16_round(rng.uniform(-1, 1, Hkv * N * d).astype(np.float32)) for _ in range(2))
+    T = lambda x, h: torch.from_numpy(x).reshape(1, h, N, d).to("cuda", torch.bfloat16)  # noqa: E731
+    out, lse = s2.s2_attn_fwd(s2.Plan.from_config(cfg), T(q, H), T(k, Hkv), T(v, Hkv))
+    torch.cuda.synchronize()
+    rp, ci = oracle.csr_all(cfg)
+    ro, rl = oracle.attn_fwd(q, k, v, rp, ci, 1, H, Hkv, N, d, S)
+    np.testing.assert_allclose(out.float().cpu().numpy().ravel(), ro, rtol=1e-2, atol=1e-2)
+    np.testing.assert_allclose(lse.cpu().numpy().ravel(), rl, rtol=1e-2, atol=1e-2)
