@@ -175,10 +175,15 @@ int s2_plan_head_nnz(const s2_plan* plan, int head, int64_t* nnz);
  * tensors have the full layout above; otherwise the tensors hold only the
  * listed units, packed unit-major: q/out [num_units, H/Hkv, N, D],
  * k/v [num_units, N, D], lse [num_units, H/Hkv, N]. */
+/* Literal zero softmax scale (negative zero; +0.0 selects the default). */
+#define S2_SCALE_ZERO (-0.0)
+
 typedef struct s2_attn_args {
     int dtype;
     int batch, num_heads, num_kv_heads, seq_len, head_dim;
-    double scale; /* 0 => 1/sqrt(head_dim) as AttentionTensors::zeros */
+    double scale; /* +0.0 => 1/sqrt(head_dim) as AttentionTensors::zeros;
+                     S2_SCALE_ZERO (-0.0) => a literal 0 (uniform weights, as the
+                     reference computes for scale == 0) */
     int num_splits;
     int num_units;       /* ignored when unit_ids == NULL */
     const int* unit_ids; /* host */

@@ -136,10 +136,11 @@ def _require_cuda(*ts):
             raise _abi.S2InvalidArgument(1, "tensors must be contiguous")
 
 
-def _check_tensors(q, k, v, out=None, lse=None, dout=None, grads=(), unit_ids=None):
+def _check_tensors(q, k, v, out=None, lse=None, dout=None, grads=(), unit_ids=None, plan=None):
     """Shapes / dtypes / devices the C ABI takes on trust (it receives pointers):
     mismatches raise here instead of reading out of bounds (kernel_common.hpp:20-32's
-    size checks, for device tensors)."""
+    size checks, for device tensors).  With the plan, the head counts are checked
+    against it too (the kernels size their TMA maps and head lists from the plan)."""
     import torch
 
     def bad(msg):
@@ -156,6 +157,8 @@ def _check_tensors(q, k, v, out=None, lse=None, dout=None, grads=(), unit_ids=No
             bad("q must be [B, H, N, D] and k/v [B, Hkv, N, D]")
         if k.shape[0] != q.shape[0] or k.shape[2] != q.shape[2] or k.shape[3] != q.shape[3]:
             bad("q and k/v disagree in batch, seq_len or head_dim")
+        if plan is not None and (q.shape[1] != plan.num_heads or k.shape[1] != plan.num_kv_heads):
+            bad("q / k heads do not match the plan's num_heads / num_kv_heads")
     else:
         if q.dim() != 4 or k.dim() != 3:
             bad("with unit_ids, q must be [U, H/Hkv, N, D] and k/v [U, N, D]")
@@ -163,6 +166,8 @@ def _check_tensors(q, k, v, out=None, lse=None, dout=None, grads=(), unit_ids=No
             bad("q and k/v disagree in units, seq_len or head_dim")
         if len(unit_ids) != q.shape[0]:
             bad("len(unit_ids) must equal the packed unit dimension")
+        if plan is not None and q.shape[1] != plan.num_heads // plan.num_kv_heads:
+            bad("with unit_ids, q's second dimension must be the plan's num_heads / num_kv_heads")
     devs = {t.device for t in (q, k, v, out, lse, dout, *grads) if t is not None}
     if len(devs) != 1:
         bad("tensors live on different devices")
@@ -197,7 +202,9 @@ def _fwd_args(plan, q, k, v, out, lse, scale, num_splits, unit_ids):
     a = _abi.s2_attn_args()
     a.dtype = _dtype_code(q)
     a.batch, a.num_heads, a.num_kv_heads, a.seq_len, a.head_dim = B, H, Hkv, N, D
-    a.scale = 0.0 if scale is None else float(scale)
+    # None: 1/sqrt(D) (+0.0 in the ABI); an explicit 0 is the reference's literal
+    # zero scale (uniform weights), S2_SCALE_ZERO = -0.0
+    a.scale = 0.0 if scale is None else (-0.0 if float(scale) == 0.0 else float(scale))
     a.num_splits = num_splits
     a.num_units = nu
     a.unit_ids = uptr
@@ -218,7 +225,7 @@ def s2_attn_fwd(plan: Plan, q, k, v, *, scale: Optional[float] = None, num_split
     if lse is None:
         lse = torch.empty(q.shape[:-1], device=q.device, dtype=torch.float32)
     _require_cuda(out, lse)
-    _check_tensors(q, k, v, out, lse, unit_ids=unit_ids)
+    _check_tensors(q, k, v, out, lse, unit_ids=unit_ids, plan=plan)
     a, keep = _fwd_args(plan, q, k, v, out, lse, scale, num_splits, unit_ids)
     check(lib().s2_attn_fwd(plan.handle, ctypes.byref(a), _stream_ptr(stream)))
     return out, lse
@@ -241,7 +248,7 @@ def s2_attn_fwd_peers(plan: Plan, q, k, v, *, unit_ids, peer_out, peer_lse, unit
     if lse is None:
         lse = torch.empty(q.shape[:-1], device=q.device, dtype=torch.float32)
     _require_cuda(out, lse)
-    _check_tensors(q, k, v, out, lse, unit_ids=unit_ids)
+    _check_tensors(q, k, v, out, lse, unit_ids=unit_ids, plan=plan)
     full = (int(total_units),) + tuple(q.shape[1:])
     for po_, pl_ in zip(peer_out, peer_lse):
         if tuple(po_.shape) != full or po_.dtype != q.dtype or tuple(pl_.shape) != full[:-1]:
@@ -270,7 +277,7 @@ def s2_attn_bwd(plan: Plan, q, k, v, out, lse, dout, *, scale: Optional[float] =
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
     _require_cuda(dq, dk, dv)
-    _check_tensors(q, k, v, out, lse, dout, (dq, dk, dv), unit_ids=unit_ids)
+    _check_tensors(q, k, v, out, lse, dout, (dq, dk, dv), unit_ids=unit_ids, plan=plan)
     fa, keep = _fwd_args(plan, q, k, v, out, lse, scale, 1, unit_ids)
     a = _abi.s2_attn_bwd_args()
     a.fwd = fa

@@ -71,6 +71,8 @@ static std::string check_cfg_ptr(const s2_pattern_config* cfg) {
     } while (0)
 
 int ensure_csr_uploaded(s2_plan* p) {
+    if (int rc = check_device(p)) return rc;
+    if (p->device < 0) cudaGetDevice(&p->device);
     if (p->csr_uploaded) return S2_OK;
     const int H = p->num_heads, B = p->num_blocks;
     std::vector<int> rp(static_cast<size_t>(H) * (B + 1));
@@ -89,7 +91,20 @@ int ensure_csr_uploaded(s2_plan* p) {
     return S2_OK;
 }
 
+int check_device(const s2_plan* p) {
+    if (p->device < 0) return S2_OK;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != p->device)
+        return fail(S2_ERR_INVALID_ARGUMENT, "plan was first used on device " + std::to_string(p->device) +
+                                                 "; its device-side lists cannot serve device " +
+                                                 std::to_string(cur) + " (create one plan per device)");
+    return S2_OK;
+}
+
 Lists* get_lists(s2_plan* p, int seq_len, int* status) {
+    if ((*status = check_device(p)) != S2_OK) return nullptr;
+    if (p->device < 0) cudaGetDevice(&p->device);
     auto it = p->lists.find(seq_len);
     Lists* L;
     if (it == p->lists.end()) {
@@ -275,7 +290,20 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
             }
             halves[t.offset] = h;
         }
-        for (auto& it : bi) it.nsteps = static_cast<int32_t>(halves.at(it.offset) * hpg);
+        // 128-row kernel: q tiles with a mask bit in either chunk
+        std::unordered_map<int64_t, int64_t> tiles;
+        for (const BwdTile& t : L->bwd.tiles) {
+            int64_t n = 0;
+            for (int e = 0; e < t.count; ++e) {
+                const BwdEntry& en = L->bwd.entries[t.offset + e];
+                n += (en.mask0 | en.mask1) != 0;
+            }
+            tiles[t.offset] = n;
+        }
+        for (auto& it : bi) {
+            it.nsteps = static_cast<int32_t>(halves.at(it.offset) * hpg);
+            it.nsteps128 = static_cast<int32_t>(tiles.at(it.offset) * hpg);
+        }
         const size_t nb_all = bi.size();
         bi.erase(std::remove_if(bi.begin(), bi.end(), [](const s2dev::BwdItem& a) { return a.nsteps == 0; }),
                  bi.end());
@@ -581,9 +609,11 @@ int s2_plan_fwd_tiles(s2_plan* p, int* num_qtiles, int64_t* num_entries, int64_t
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->lists.find(p->seq_len);
     if (it == p->lists.end()) {
+        // the same complete entry get_lists() builds (a later forward reuses it)
         auto nl = std::make_unique<Lists>();
         nl->tiled = true;
         nl->fwd = build_fwd_list(p->csr, p->seq_len, p->block_size);
+        nl->pairs = build_pair_list(nl->fwd, p->num_heads);
         nl->bwd = build_bwd_list(nl->fwd, p->num_heads, p->num_kv_heads, p->seq_len);
         it = p->lists.emplace(p->seq_len, std::move(nl)).first;
     }
@@ -671,7 +701,7 @@ static int attn_fwd_impl(s2_plan* p, const s2_attn_args* a, int num_peers, void*
     if (int rc = check_args(p, a)) return rc;
     std::lock_guard<std::mutex> lk(p->mu);
     const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const double scale = a->scale != 0.0 ? a->scale : 1.0 / std::sqrt(double(a->head_dim));
+    const double scale = resolve_scale(a->scale, a->head_dim);
     const int hpg = p->num_heads / p->num_kv_heads;
     int rc = S2_OK;
     Lists* L = get_lists(p, a->seq_len, &rc);
@@ -685,9 +715,10 @@ static int attn_fwd_impl(s2_plan* p, const s2_attn_args* a, int num_peers, void*
     if (use_tcgen05(p, a)) {
         try {
             const uint64_t N = a->seq_len, D = a->head_dim;
-            const CUtensorMap mq = s2host::make_map_bf16_3d(a->q, D, N, uint64_t(nu) * hpg, 64, 128);
-            const CUtensorMap mk = s2host::make_map_bf16_3d(a->k, D, N, nu, 64, 64);
-            const CUtensorMap mv = s2host::make_map_bf16_3d(a->v, D, N, nu, 64, 64);
+            // loads: whole-row 4-D boxes (one TMA per 128-row Q tile / 64-key chunk)
+            const CUtensorMap mq = s2host::make_map_bf16_kmajor(a->q, D, N, uint64_t(nu) * hpg, 128);
+            const CUtensorMap mk = s2host::make_map_bf16_kmajor(a->k, D, N, nu, 64);
+            const CUtensorMap mv = s2host::make_map_bf16_kmajor(a->v, D, N, nu, 64);
             const CUtensorMap mo = s2host::make_map_bf16_3d(a->out, D, N, uint64_t(nu) * hpg, 64, 128);
             CUtensorMap peer_maps[8];
             for (int r = 0; r < num_peers; ++r)

@@ -1,5 +1,6 @@
 // C ABI: backward (dQ over the CSR tile list, dK/dV over the transposed list).
 #include <cmath>
+#include <cstdlib>
 
 #include "capi_internal.hpp"
 #include "tma_host.hpp"
@@ -11,7 +12,8 @@ cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CU
                                 const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o0,
                                 const CUtensorMap& o1, const void* items, const int* sched, int grid,
                                 const void* entries, const float* lse2, const float* delta,
-                                int N, int Npad, int hpg, float scale, cudaStream_t stream);
+                                int N, int Npad, int hpg, float scale, cudaStream_t stream,
+                                void* g0, void* g1);
 
 using namespace s2;
 
@@ -62,7 +64,7 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
     const int nkv = nqbh / hpg;
     const int N = f.seq_len, D = f.head_dim;
     const int Npad = (N + 127) / 128 * 128;
-    const double scale = f.scale != 0.0 ? f.scale : 1.0 / std::sqrt(double(D));
+    const double scale = resolve_scale(f.scale, D);
     float* delta = static_cast<float*>(workspace);
     float* lse2 = delta + static_cast<size_t>(nqbh) * Npad;
     cudaError_t e;
@@ -75,12 +77,18 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
     if (e != cudaSuccess) return cuda_fail(e, "s2_attn_bwd prep launch");
     try {
         using s2host::make_map_bf16_3d;
-        const CUtensorMap q64 = make_map_bf16_3d(f.q, D, N, nqbh, 64, 64);
-        const CUtensorMap do64 = make_map_bf16_3d(a->dout, D, N, nqbh, 64, 64);
-        const CUtensorMap q128 = make_map_bf16_3d(f.q, D, N, nqbh, 64, 128);
-        const CUtensorMap do128 = make_map_bf16_3d(a->dout, D, N, nqbh, 64, 128);
+        using s2host::make_map_bf16_kmajor;
+        // streamed operands: whole-row 4-D boxes (Q/dO halves for dK/dV, Q/dO tiles
+        // and K/V chunks for dQ); the dK/dV kernel's K/V pair tiles and the 128-key
+        // dQ kernel's K/V stages are two chunks per D/64 slice: 3-D boxes
+        const CUtensorMap q64 = make_map_bf16_kmajor(f.q, D, N, nqbh, 64);
+        const CUtensorMap do64 = make_map_bf16_kmajor(a->dout, D, N, nqbh, 64);
+        const CUtensorMap q128 = make_map_bf16_kmajor(f.q, D, N, nqbh, 128);
+        const CUtensorMap do128 = make_map_bf16_kmajor(a->dout, D, N, nqbh, 128);
         const CUtensorMap mk = make_map_bf16_3d(f.k, D, N, nkv, 64, 64);
         const CUtensorMap mv = make_map_bf16_3d(f.v, D, N, nkv, 64, 64);
+        const CUtensorMap mk4 = make_map_bf16_kmajor(f.k, D, N, nkv, 64);
+        const CUtensorMap mv4 = make_map_bf16_kmajor(f.v, D, N, nkv, 64);
         // key chunks no query attends are never visited (no tile covers them, or a
         // tile has no steps): their dK / dV are 0
         if (w->bwd_dropped || L->bwd.uncovered) {
@@ -94,13 +102,28 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
         const CUtensorMap mdq = make_map_bf16_3d(a->dq, D, N, nqbh, 64, 128);
         {
             ProfScope prof("bwd_dkv_sm100", st);
-            e = s2_launch_bwd_sm100(0, D, q64, do64, mk, mv, mdk, mdv, w->bwd.ptr, w->bwd_sched.as<int>(),
-                                    w->grid, L->d_entries.ptr, lse2, delta, N, Npad, hpg, float(scale), st);
+            // S2_DKV_V2=1: the experimental 128-row-step dK/dV kernel (s2_bwd_dkv2_kernel;
+            // slower at cfg3)
+            const char* dkv_env = std::getenv("S2_DKV_V2");
+            const bool dkv_v1 = !(dkv_env && dkv_env[0] == '1');
+            if (dkv_v1)
+                e = s2_launch_bwd_sm100(0, D, q64, do64, mk, mv, mdk, mdv, w->bwd.ptr, w->bwd_sched.as<int>(),
+                                        w->grid, L->d_entries.ptr, lse2, delta, N, Npad, hpg, float(scale), st,
+                                        nullptr, nullptr);
+            else
+                e = s2_launch_bwd_sm100(3, D, q128, do128, mk, mv, mdk, mdv, w->bwd.ptr, w->bwd_sched.as<int>(),
+                                        w->grid, L->d_entries.ptr, lse2, delta, N, Npad, hpg, float(scale), st,
+                                        a->dk, a->dv);
         }
         if (e == cudaSuccess) {
             ProfScope prof("bwd_dq_sm100", st);
-            e = s2_launch_bwd_sm100(1, D, q128, do128, mk, mv, mdq, mdq, w->fwd.ptr, w->fwd_sched.as<int>(),
-                                    w->grid, L->d_chunks.ptr, lse2, delta, N, Npad, hpg, float(scale), st);
+            // S2_DQ_V2=1: the experimental 128-key-step dQ kernel (s2_bwd_dq2_kernel;
+            // slower at cfg3: its two-chunk K/V stages need 8 KB TMA boxes)
+            const char* dq_env = std::getenv("S2_DQ_V2");
+            const bool dq_v1 = !(dq_env && dq_env[0] == '1');
+            e = s2_launch_bwd_sm100(dq_v1 ? 1 : 2, D, q128, do128, dq_v1 ? mk4 : mk, dq_v1 ? mv4 : mv, mdq, mdq, w->fwd.ptr, w->fwd_sched.as<int>(),
+                                    w->grid, L->d_chunks.ptr, lse2, delta, N, Npad, hpg, float(scale), st,
+                                    nullptr, nullptr);
         }
     } catch (const std::exception& ex) {
         return fail(S2_ERR_CUDA, ex.what());

@@ -260,7 +260,7 @@ int s2_attn_decode(s2_kvcache* c, const void* q, void* out, float* lse, double s
         max_len = std::max<int>(max_len, static_cast<int>(c->row_ptr[static_cast<size_t>(g) * (c->NB + 1) + bt + 1] -
                                                           c->row_ptr[static_cast<size_t>(g) * (c->NB + 1) + bt]));
     const int splits = choose_splits(c, max_len);
-    const double sc = scale != 0.0 ? scale : 1.0 / std::sqrt(double(c->D));
+    const double sc = resolve_scale(scale, c->D);
     float* o_part = static_cast<float*>(workspace);
     float* lse_part = o_part + static_cast<size_t>(c->batch) * c->H * kMaxSplits * c->D;
     s2dev::DecodeParams p{static_cast<const __nv_bfloat16*>(q), c->d_row_ptr.as<int64_t>(),

@@ -21,7 +21,7 @@ struct BwdItem {
     int32_t count;   // q tiles visited
     int64_t offset;  // into the BwdEntry array
     int32_t nsteps;  // (query head, q tile, active 64-row half) steps = hpg * active halves
-    int32_t pad;
+    int32_t nsteps128;  // (query head, q tile) steps of the 128-row kernel = hpg * active tiles
 };
 struct BwdEntry {
     int32_t qtile;

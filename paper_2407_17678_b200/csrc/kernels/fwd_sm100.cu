@@ -204,9 +204,7 @@ __global__ void __launch_bounds__(384, 1)
                     if (q_use[t] > 0) mbar_wait(smem_u32(&bar_qe[t]), (q_use[t] - 1) & 1);
                     const uint32_t sQ = sQ0 + t * C::kQBytes;
                     mbar_expect_tx(smem_u32(&bar_qf[t]), C::kQBytes);
-                    for (int s = 0; s < C::kSub; ++s)
-                        tma_load_3d(sQ + s * 16384, &tmQ, smem_u32(&bar_qf[t]), s * 64,
-                                    (2 * it.qpair + t) * 128, it.bh);
+                    tma_load_rows(sQ, &tmQ, smem_u32(&bar_qf[t]), (2 * it.qpair + t) * 128, it.bh);
                     ++q_use[t];
                 }
                 const PairStep* steps = p.steps + it.step_off;
@@ -220,10 +218,8 @@ __global__ void __launch_bounds__(384, 1)
                         const uint32_t sK = sKV + st * C::kStageBytes, sV = sK + C::kCBytes;
                         const uint32_t bar = smem_u32(&bar_kf[st]);
                         mbar_expect_tx(bar, 2 * C::kCBytes);
-                        for (int sb = 0; sb < C::kSub; ++sb) {
-                            tma_load_3d_hint(sK + sb * 8192, &tmK, bar, sb * 64, chunk * 64, kvbh, keep);
-                            tma_load_3d_hint(sV + sb * 8192, &tmV, bar, sb * 64, chunk * 64, kvbh, keep);
-                        }
+                        tma_load_rows_hint(sK, &tmK, bar, chunk * 64, kvbh, keep);
+                        tma_load_rows_hint(sV, &tmV, bar, chunk * 64, kvbh, keep);
                         ++kv_it;
                     }
                 }

@@ -85,6 +85,24 @@ __device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap
         "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
         : "memory");
 }
+// 4-D box {64, rows, slices, 1} of a make_map_bf16_kmajor map: full rows at
+// (row, outer), landing as [slices][rows][64] SW128.
+__device__ __forceinline__ void tma_load_rows(uint32_t dst, const CUtensorMap* m, uint32_t bar, int row,
+                                              int outer) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(0), "r"(row), "r"(0), "r"(outer)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_rows_hint(uint32_t dst, const CUtensorMap* m, uint32_t bar, int row,
+                                                   int outer, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(0), "r"(row), "r"(0), "r"(outer), "l"(policy)
+        : "memory");
+}
 // TMA store shared -> global (bulk-group completion), and its group fences.
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2) {
     asm volatile(

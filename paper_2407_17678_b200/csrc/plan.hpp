@@ -76,5 +76,6 @@ struct s2_plan {
     s2::DevBuf d_row_ptr, d_col_idx, d_col_off;
     bool csr_uploaded = false;
     std::mutex mu;
+    int device = -1;  // CUDA device of the first call that built device-side state
     std::map<int, std::unique_ptr<s2::Lists>> lists;  // keyed by seq_len
 };

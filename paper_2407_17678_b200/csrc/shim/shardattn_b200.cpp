@@ -109,7 +109,7 @@ void gpu_forward(AttentionTensors& t, const std::vector<CsrMask>& csr, int block
     a.num_kv_heads = t.num_heads;
     a.seq_len = t.seq_len;
     a.head_dim = t.head_dim;
-    a.scale = t.scale;
+    a.scale = t.scale == 0.0 ? S2_SCALE_ZERO : t.scale;  // the reference applies scale literally
     a.num_splits = num_splits;
     a.q = q.p;
     a.k = k.p;
@@ -427,7 +427,7 @@ void streaming_sharded_attention_backward(const AttentionTensors& t,
     a.fwd.num_kv_heads = t.num_heads;
     a.fwd.seq_len = t.seq_len;
     a.fwd.head_dim = t.head_dim;
-    a.fwd.scale = t.scale;
+    a.fwd.scale = t.scale == 0.0 ? S2_SCALE_ZERO : t.scale;
     a.fwd.num_splits = 1;
     a.fwd.q = q.p;
     a.fwd.k = k.p;

@@ -112,7 +112,7 @@ class KVCache:
             self._ws = torch.empty(max(self._ws_bytes, 16), dtype=torch.uint8, device=q.device)
         check(lib().s2_attn_decode(self._h, ctypes.c_void_p(q.data_ptr()),
                                    ctypes.c_void_p(out.data_ptr()),
-                                   ctypes.c_void_p(lse.data_ptr()), 0.0 if scale is None else scale,
+                                   ctypes.c_void_p(lse.data_ptr()), 0.0 if scale is None else (-0.0 if scale == 0 else scale),
                                    ctypes.c_void_p(self._ws.data_ptr()), self._ws_bytes,
                                    _stream_ptr(stream)))
         return out, lse

@@ -19,6 +19,7 @@ Two `torch.library` custom ops wrap the C ABI (include/s2attn.h):
 There is no CPU implementation: on a CPU tensor the op raises (the product
 path has no CPU fallback)."""
 import itertools
+import math
 import weakref
 from typing import Tuple
 
@@ -48,7 +49,8 @@ def _plan(pid: int):
 
 
 def _opt_scale(scale: float):
-    return None if scale == 0.0 else scale
+    # +0.0 encodes "default 1/sqrt(D)"; -0.0 an explicit zero (S2_SCALE_ZERO)
+    return None if (scale == 0.0 and math.copysign(1.0, scale) > 0) else scale
 
 
 @torch.library.custom_op("s2attn::fwd", mutates_args=())
@@ -86,6 +88,9 @@ def _setup_context(ctx, inputs, output):
     out, lse = output
     ctx.save_for_backward(q, k, v, out, lse)
     ctx.pid, ctx.scale = pid, scale
+    # the registry holds plans weakly: keep this one alive as long as the graph
+    # (s2_attention(q, k, v, Plan.from_config(cfg)) passes a temporary)
+    ctx.plan = _plan(pid)
     ctx.set_materialize_grads(True)
 
 
@@ -102,4 +107,5 @@ s2attn_fwd.register_autograd(_backward, setup_context=_setup_context)
 
 def s2_attention(q, k, v, plan, scale=None):
     """Differentiable S2 attention through the registered ops: out [B,H,N,D]."""
-    return torch.ops.s2attn.fwd(q, k, v, plan_id(plan), 0.0 if scale is None else float(scale))[0]
+    return torch.ops.s2attn.fwd(q, k, v, plan_id(plan),
+                                0.0 if scale is None else (float(scale) if scale != 0 else -0.0))[0]
