@@ -52,9 +52,10 @@ enum {
     S2_ERR_BUFFER_TOO_SMALL = 7
 };
 
-/* SMs the persistent tcgen05 kernels leave free for concurrent work (e.g.
- * NCCL's all-gather CTAs on a communication stream overlapping the
- * backward): their grid becomes (SM count - sms).  Process-wide; 0 default. */
+/* SMs the persistent backward kernels (dK/dV, dQ) leave free for concurrent
+ * work: NCCL's all-gather of O on a communication stream overlaps the
+ * backward, so their grid becomes (SM count - sms).  The forward, which has no
+ * collective to overlap, keeps every SM.  Process-wide; 0 default. */
 int s2_set_sm_reserve(int sms);
 
 /* Message for the last non-zero status returned on this thread. */
@@ -283,6 +284,14 @@ int s2_partition_lpt(int num_units, const int64_t* weights, int num_ranks, int* 
 /* 4 * head_dim * block_size^2 per active pair, summed over heads and batch. */
 int s2_plan_fwd_flops(const s2_plan* plan, int batch, int head_dim, double* active_flops,
                       double* dense_causal_flops);
+
+/* ---- reference test inputs ---------------------------------------------- */
+/* AttentionTensors::random (attention.cpp:135-144): mt19937_64(seed), U[-1,1]
+ * floats from std::uniform_real_distribution<float>, q then k then v, each
+ * num_heads * seq_len * head_dim values [H, N, d].  Host buffers; the same
+ * stream as the reference for the same seed (libstdc++). */
+int s2_random_tensors(int num_heads, int seq_len, int head_dim, uint64_t seed, float* q, float* k,
+                      float* v);
 
 /* ---- device memory helpers (so FFI callers need no CUDA runtime) --------- */
 int s2_device_count(int* count);

@@ -6,6 +6,7 @@
 //     the reference's mask validation (dense: finiteness + causal masks)
 // Extensions in the house style (the reference has neither):
 //   streaming_sharded_attention_backward -> tcgen05 bf16 backward kernels
+//   sharded_decode -> compacted KV cache + split-KV decode kernel
 #pragma once
 
 #include <cstdint>
@@ -54,5 +55,18 @@ struct AttentionGrads {
 void streaming_sharded_attention_backward(const AttentionTensors& t,
                                           const std::vector<CsrMask>& csr, int block_size,
                                           const std::vector<float>& dout, AttentionGrads& grads);
+
+/// Decode of one token position: row `position` of every head, computed the
+/// way a generation step would -- the keys/values of tokens 0..position are
+/// compacted into a per-head cache that keeps only the blocks some row at or
+/// after `position` can still attend (analysis.cpp:57-104's retained set), and
+/// one query row per head attends the blocks of its mask row (reference.cpp:28-50
+/// for a single row), tokens <= position.  Equals row `position` of
+/// streaming_sharded_attention within bf16 tolerance (inputs rounded to bf16).
+/// Resizes out / lse like the forward (zeros / -inf) and fills only that row.
+/// Throws std::invalid_argument on the forward's conditions and on a position
+/// outside [0, seq_len).
+void sharded_decode(AttentionTensors& t, const std::vector<CsrMask>& csr, int block_size,
+                    int position);
 
 }  // namespace shardattn

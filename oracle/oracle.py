@@ -30,15 +30,46 @@ _IP = ctypes.POINTER(ctypes.c_int)
 _I64P = ctypes.POINTER(ctypes.c_int64)
 
 
+S2_MAX_SEGMENTS = 8  # include/s2attn.h
+
+
+class _Segment(ctypes.Structure):
+    """Mirror of include/s2attn.h's s2_stride_segment (POD), so the oracle needs
+    nothing from the product package (bench.py's reference arm imports none of it)."""
+    _fields_ = [("start_block_distance", ctypes.c_int), ("end_block_distance", ctypes.c_int),
+                ("stride", ctypes.c_int), ("num_offsets", ctypes.c_int),
+                ("offsets", ctypes.POINTER(ctypes.c_int))]
+
+
+class PatternC(ctypes.Structure):
+    """Mirror of include/s2attn.h's s2_pattern_config (the reference's PatternConfig
+    as a POD, pattern.hpp:37-60)."""
+    _fields_ = [("seq_len", ctypes.c_int), ("block_size", ctypes.c_int),
+                ("num_heads", ctypes.c_int), ("num_kv_heads", ctypes.c_int),
+                ("local_blocks", ctypes.c_int), ("local_stride", ctypes.c_int),
+                ("num_segments", ctypes.c_int), ("segments", _Segment * S2_MAX_SEGMENTS)]
+
+
+def single_stride(seq_len, block_size, num_heads, local_blocks, vert_stride, num_kv_heads=0):
+    """make_single_stride_config (pattern.cpp:190-204) as the C struct: one segment
+    {local_blocks, num_blocks, vert_stride} with the default head offsets."""
+    c = PatternC()
+    c.seq_len, c.block_size, c.num_heads = seq_len, block_size, num_heads
+    c.num_kv_heads = num_kv_heads if num_kv_heads > 0 else num_heads
+    c.local_blocks, c.local_stride = local_blocks, 1
+    B = (seq_len + block_size - 1) // block_size
+    if local_blocks < B:
+        c.num_segments = 1
+        c.segments[0].start_block_distance = local_blocks
+        c.segments[0].end_block_distance = B
+        c.segments[0].stride = vert_stride
+    return c
+
+
 def _cfg_type():
-    import sys
-
-    root = os.path.dirname(HERE)
-    if root not in sys.path:
-        sys.path.insert(0, root)
-    from paper_2407_17678_b200._abi import s2_pattern_config
-
-    return ctypes.POINTER(s2_pattern_config)
+    # configs travel as pointers: the product's s2_pattern_config (tests) or PatternC
+    # (same layout) both pass through ctypes.byref
+    return ctypes.c_void_p
 
 
 def build_port():
@@ -81,6 +112,7 @@ def port():
                                                            _F, _F]),
             "s2o_max_rel_f": (ctypes.c_double, [_F, _F, ctypes.c_int64]),
             "s2o_max_rel_d": (ctypes.c_double, [_D, _D, ctypes.c_int64]),
+            "s2o_fnv1a64_u32": (ctypes.c_uint64, [ctypes.c_void_p, ctypes.c_int64]),
         }
         for n, (r, a) in sig.items():
             f = getattr(L, n)
@@ -161,6 +193,32 @@ def csr_all(cfg):
         rps.append(rp)
         cis.append(ci[:n])
     return np.concatenate(rps), np.concatenate(cis) if cis else np.zeros(0, np.int32)
+
+
+def csr_all_c(c):
+    """Concatenated row_ptr [H*(B+1)] / col_idx of every head of a PatternC: the
+    reference's own to_csr(build_all_masks) when oracle/_ref is built, else the
+    port.  Returns (row_ptr, col_idx, kind)."""
+    H = c.num_heads
+    B = (c.seq_len + c.block_size - 1) // c.block_size
+    R = ref()
+    if R is not None:
+        nnz = ctypes.c_int64()
+        assert R.ref_build_all_csr(ctypes.byref(c), None, None, ctypes.byref(nnz)) == 0
+        rp = np.zeros(H * (B + 1), np.int32)
+        ci = np.zeros(max(nnz.value, 1), np.int32)
+        assert R.ref_build_all_csr(ctypes.byref(c), ip(rp), ip(ci), ctypes.byref(nnz)) == 0
+        return rp, ci[:nnz.value], "reference"
+    L = port()
+    rps, cis = [], []
+    for h in range(H):
+        n = L.s2o_build_csr(ctypes.byref(c), h, None, None)
+        rp = np.zeros(B + 1, np.int32)
+        ci = np.zeros(max(n, 1), np.int32)
+        L.s2o_build_csr(ctypes.byref(c), h, ip(rp), ip(ci))
+        rps.append(rp)
+        cis.append(ci[:n])
+    return np.concatenate(rps), np.concatenate(cis), "port"
 
 
 def random_tensors(H, N, d, seed):

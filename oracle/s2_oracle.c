@@ -790,3 +790,12 @@ double s2o_max_rel_d(const double* a, const double* b, int64_t n) {
     }
     return worst;
 }
+
+/* FNV-1a 64 over 32-bit words (test infrastructure: fingerprint of a CSR array,
+ * the same fold as oracle/make_golden.py::fnv_fast; C so 128K layouts of every
+ * head are fingerprinted in milliseconds). */
+uint64_t s2o_fnv1a64_u32(const uint32_t* a, int64_t n) {
+    uint64_t h = 0xCBF29CE484222325ull;
+    for (int64_t i = 0; i < n; ++i) h = (h ^ (uint64_t)a[i]) * 0x100000001B3ull;
+    return h;
+}

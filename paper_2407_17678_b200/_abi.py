@@ -137,6 +137,8 @@ SIGNATURES = {
     "s2_partition_lpt": (_I, [_I, _I64P, _I, _IP, _I64P]),
     "s2_plan_fwd_flops": (_I, [_P, _I, _I, ctypes.POINTER(ctypes.c_double),
                                ctypes.POINTER(ctypes.c_double)]),
+    "s2_random_tensors": (_I, [_I, _I, _I, ctypes.c_uint64, ctypes.POINTER(ctypes.c_float),
+                              ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
     "s2_device_count": (_I, [_IP]),
     "s2_device_malloc": (_I, [ctypes.POINTER(_P), ctypes.c_size_t]),
     "s2_device_free": (_I, [_P]),

@@ -355,14 +355,12 @@ class AttentionTensors:
 
     @staticmethod
     def random(num_heads, seq_len, head_dim, seed) -> "AttentionTensors":
-        """U[-1,1] inputs (the reference's distribution, attention.cpp:135-144; the
-        reference's exact mt19937_64 stream lives in the test oracle)."""
+        """The reference's inputs for `seed` (attention.cpp:135-144): mt19937_64,
+        U[-1,1] floats, q then k then v (s2_random_tensors: the same stream)."""
         t = AttentionTensors.zeros(num_heads, seq_len, head_dim)
-        rng = np.random.default_rng(seed)
-        n = t.q.size
-        t.q[:] = rng.uniform(-1, 1, n)
-        t.k[:] = rng.uniform(-1, 1, n)
-        t.v[:] = rng.uniform(-1, 1, n)
+        fp = ctypes.POINTER(ctypes.c_float)
+        check(lib().s2_random_tensors(num_heads, seq_len, head_dim, int(seed) & (2**64 - 1),
+                                      t.q.ctypes.data_as(fp), t.k.ctypes.data_as(fp), t.v.ctypes.data_as(fp)))
         return t
 
     def idx(self, head, token, component) -> int:

@@ -202,8 +202,10 @@ static int64_t sched_overhead(const char* env, int64_t dflt) {
 // ui-th listed unit is ui*hpg + j (= b*H + h when every unit is listed).
 WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* unit_ids,
                      int* status) {
-    const int grid = persistent_grid();
-    std::string key = std::to_string(batch) + ":g" + std::to_string(grid) + ":";
+    // the forward fills every SM; the backward kernels leave s2_set_sm_reserve SMs
+    // to the collective that overlaps them (the all-gather of O)
+    const int grid_fwd = num_sms(), grid = persistent_grid();
+    std::string key = std::to_string(batch) + ":g" + std::to_string(grid_fwd) + "/" + std::to_string(grid) + ":";
     std::vector<int> units;
     if (unit_ids) {
         units.assign(unit_ids, unit_ids + num_units);
@@ -263,7 +265,7 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
                               2 * q + 1 < nt ? 1 : 0, off});
             }
         const std::vector<int32_t> off_pair = schedule_items(
-            pi, grid, [](const PairItem& a) { return int64_t(a.nsteps) * (1 + a.has_b); },
+            pi, grid_fwd, [](const PairItem& a) { return int64_t(a.nsteps) * (1 + a.has_b); },
             [](const PairItem& a) { return a.bh; }, sched_overhead("S2_SCHED_OVH_FWD", 4));
         w->num_pair = static_cast<int>(pi.size());
         if ((e = upload(w->pair, pi.data(), pi.size() * sizeof(PairItem))) != cudaSuccess ||
@@ -315,6 +317,7 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
         w->num_fwd = static_cast<int>(fi.size());
         w->num_bwd = static_cast<int>(bi.size());
         w->grid = grid;
+        w->grid_fwd = grid_fwd;
         if ((e = upload(w->fwd, fi.data(), fi.size() * sizeof(s2dev::FwdItem))) != cudaSuccess ||
             (e = upload(w->bwd, bi.data(), bi.size() * sizeof(s2dev::BwdItem))) != cudaSuccess ||
             (e = upload(w->bwd_sched, off_bwd.data(), off_bwd.size() * sizeof(int32_t))) != cudaSuccess) {
@@ -725,7 +728,7 @@ static int attn_fwd_impl(s2_plan* p, const s2_attn_args* a, int num_peers, void*
                 peer_maps[r] = s2host::make_map_bf16_3d(peer_out[r], D, N, uint64_t(total_units) * hpg, 64, 128);
             ProfScope prof("fwd_sm100", st);
             e = s2_launch_fwd_sm100(a->head_dim, mq, mk, mv, mo, w->pair.ptr, w->pair_sched.as<int>(),
-                                    w->grid, L->d_steps.ptr, static_cast<__nv_bfloat16*>(a->out),
+                                    w->grid_fwd, L->d_steps.ptr, static_cast<__nv_bfloat16*>(a->out),
                                     a->lse, a->seq_len, hpg, float(scale * M_LOG2E), st, num_peers,
                                     unit_global, peer_lse, peer_maps);
         } catch (const std::exception& ex) {

@@ -46,7 +46,8 @@ struct WorkItems {
     int num_bwd = 0;
     bool bwd_dropped = false;  // key tiles nobody attends (user CSR without diagonal): dK/dV = 0
     DevBuf fwd_sched, pair_sched, bwd_sched;  // int[grid + 1] per-CTA item ranges
-    int grid = 0;
+    int grid = 0;      // backward kernels (dQ: fwd_sched, dK/dV: bwd_sched): SMs minus the reserve
+    int grid_fwd = 0;  // forward (pair_sched): every SM
     DevBuf simt_bh;   // int[num_bh] data index
     DevBuf simt_head; // int[num_bh] layout head
     int num_bh = 0;

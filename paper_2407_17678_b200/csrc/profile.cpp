@@ -1,6 +1,8 @@
 // Per-kernel CUDA-event timing for bench.py (s2_profile_* in s2attn.h).
 #include <cuda_runtime.h>
 
+#include <random>
+
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -95,6 +97,19 @@ int s2_profile_collect(int max_kernels, char* names, double* total_ms, int* laun
 }
 
 extern "C" {
+int s2_random_tensors(int num_heads, int seq_len, int head_dim, uint64_t seed, float* q, float* k,
+                      float* v) {
+    if (num_heads < 1 || seq_len < 1 || head_dim < 1)
+        return fail(S2_ERR_INVALID_ARGUMENT, "tensor dimensions must be positive");
+    if (!q || !k || !v) return fail(S2_ERR_INVALID_ARGUMENT, "null argument");
+    const size_t n = static_cast<size_t>(num_heads) * seq_len * head_dim;
+    std::mt19937_64 gen(seed);
+    std::uniform_real_distribution<float> u(-1.0f, 1.0f);
+    for (float* dst : {q, k, v})
+        for (size_t i = 0; i < n; ++i) dst[i] = u(gen);
+    return S2_OK;
+}
+
 int s2_device_count(int* count) {
     if (!count) return fail(S2_ERR_INVALID_ARGUMENT, "null argument");
     int n = 0;

@@ -455,4 +455,64 @@ void streaming_sharded_attention_backward(const AttentionTensors& t,
     grads.dv = from_bf16(r);
 }
 
+void sharded_decode(AttentionTensors& t, const std::vector<CsrMask>& csr, int block_size, int position) {
+    if (csr.empty()) throw std::invalid_argument("csr list is empty");
+    check_shapes(t, csr.size(), csr.front().num_blocks, block_size);
+    for (const CsrMask& c : csr) {
+        c.validate();
+        if (c.num_blocks != csr.front().num_blocks)
+            throw std::invalid_argument("csr masks differ in block count");
+    }
+    if (position < 0 || position >= t.seq_len)
+        throw std::invalid_argument("decode position outside [0, seq_len)");
+    auto bf16 = [](float x) {
+        uint32_t u;
+        std::memcpy(&u, &x, 4);
+        return static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+    };
+    const int H = t.num_heads, d = t.head_dim, T = position + 1;
+    Plan plan = make_plan(csr, t.seq_len, block_size);
+    struct Cache {
+        s2_kvcache* c = nullptr;
+        ~Cache() { s2_kvcache_destroy(c); }
+    } cache;
+    ck(s2_kvcache_create(plan.p, 1, d, S2_DTYPE_BF16, &cache.c));
+    // the prefix [H, T, d] of k / v, bf16
+    const size_t nkv = static_cast<size_t>(H) * T * d;
+    std::vector<uint16_t> hk(nkv), hv(nkv), hq(static_cast<size_t>(H) * d);
+    for (int h = 0; h < H; ++h)
+        for (int s = 0; s < T; ++s)
+            for (int c = 0; c < d; ++c) {
+                const size_t dst = (static_cast<size_t>(h) * T + s) * d + c;
+                hk[dst] = bf16(t.k[t.idx(h, s, c)]);
+                hv[dst] = bf16(t.v[t.idx(h, s, c)]);
+            }
+    for (int h = 0; h < H; ++h)
+        for (int c = 0; c < d; ++c) hq[static_cast<size_t>(h) * d + c] = bf16(t.q[t.idx(h, position, c)]);
+    Dev k(nkv * 2), v(nkv * 2), q(hq.size() * 2), o(hq.size() * 2), l(static_cast<size_t>(H) * 4);
+    ck(s2_memcpy_h2d(k.p, hk.data(), nkv * 2, nullptr));
+    ck(s2_memcpy_h2d(v.p, hv.data(), nkv * 2, nullptr));
+    ck(s2_memcpy_h2d(q.p, hq.data(), hq.size() * 2, nullptr));
+    ck(s2_kvcache_prefill(cache.c, k.p, v.p, T, nullptr));
+    size_t ws = 0;
+    ck(s2_attn_decode_workspace_size(cache.c, &ws));
+    Dev w(ws);
+    ck(s2_attn_decode(cache.c, q.p, o.p, static_cast<float*>(l.p), t.scale == 0.0 ? S2_SCALE_ZERO : t.scale, w.p,
+                      ws, nullptr));
+    std::vector<uint16_t> ho(hq.size());
+    std::vector<float> hl(H);
+    ck(s2_memcpy_d2h(ho.data(), o.p, ho.size() * 2, nullptr));
+    ck(s2_memcpy_d2h(hl.data(), l.p, hl.size() * 4, nullptr));
+    ck(s2_stream_synchronize(nullptr));
+    t.out.assign(t.q.size(), 0.0f);
+    t.lse.assign(static_cast<size_t>(H) * t.seq_len, -std::numeric_limits<double>::infinity());
+    for (int h = 0; h < H; ++h) {
+        for (int c = 0; c < d; ++c) {
+            const uint32_t u = static_cast<uint32_t>(ho[static_cast<size_t>(h) * d + c]) << 16;
+            std::memcpy(&t.out[t.idx(h, position, c)], &u, 4);
+        }
+        t.lse[t.row_index(h, position)] = hl[h];
+    }
+}
+
 }  // namespace shardattn

@@ -219,6 +219,44 @@ int main() {
         CHECK(close(gr.dk, dk, 2e-2));
         CHECK(close(gr.dv, dv, 2e-2));
     }
+    // extension: decode of one position over the compacted cache == that row of the
+    // forward (bf16 operands: 2e-2), rows <= position only; other rows zero / -inf
+    {
+        Inst in = make(4, 1000, 128, 64, 3, 71, 2);
+        std::vector<float> ro;
+        std::vector<double> rl;
+        oracle_fwd(in, ro, rl);
+        for (int pos : {0, 63, 64, 500, 999}) {
+            AttentionTensors a = in.t;
+            sharded_decode(a, in.csr, 64, pos);
+            bool ok = true;
+            for (int h = 0; h < 4; ++h) {
+                for (int x = 0; x < 128; ++x) {
+                    const double got = a.out[a.idx(h, pos, x)], ref = ro[a.idx(h, pos, x)];
+                    ok = ok && std::fabs(got - ref) <= 2e-2 + 2e-2 * std::fabs(ref);
+                }
+                ok = ok && std::fabs(a.lse[a.row_index(h, pos)] - rl[a.row_index(h, pos)]) <= 2e-2;
+                const int other = pos == 0 ? 1 : 0;
+                ok = ok && a.out[a.idx(h, other, 0)] == 0.0f && std::isinf(a.lse[a.row_index(h, other)]);
+            }
+            CHECK(ok);
+        }
+        CHECK_THROWS(sharded_decode(in.t, in.csr, 64, 1000));
+        CHECK_THROWS(sharded_decode(in.t, in.csr, 64, -1));
+    }
+    // a literal zero scale (AttentionTensors' default member value, attention.hpp:23)
+    // is applied as given: uniform weights over the admitted keys
+    {
+        Inst in = make(2, 200, 16, 8, 3, 83);
+        in.t.scale = 0.0;
+        std::vector<float> ro;
+        std::vector<double> rl;
+        oracle_fwd(in, ro, rl);
+        AttentionTensors a = in.t;
+        streaming_sharded_attention(a, in.csr, 8);
+        CHECK(close(a.out, ro, 1e-4));
+        CHECK(close(a.lse, rl, 1e-4));
+    }
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }

@@ -41,7 +41,16 @@ def load_npz(name):
 
 
 def fnv_fast(arr) -> str:
-    """Must match oracle/make_golden.py::fnv_fast."""
+    """FNV-1a 64 over 32-bit words; must match oracle/make_golden.py::fnv_fast.
+    Folded in C by the oracle library (s2o_fnv1a64_u32) so every head of a 128K
+    layout is fingerprinted quickly; the Python fold below is its cross-check."""
+    import oracle
+
+    a = np.ascontiguousarray(arr, dtype=np.uint32)
+    return f"{oracle.port().s2o_fnv1a64_u32(a.ctypes.data, a.size):016x}"
+
+
+def fnv_py(arr) -> str:
     a = np.ascontiguousarray(arr, dtype=np.uint32).astype(np.uint64)
     h = 0xCBF29CE484222325
     prime = 0x100000001B3

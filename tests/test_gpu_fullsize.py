@@ -138,6 +138,46 @@ def test_cfg5_128k_forward_rows_match_oracle():
         np.testing.assert_allclose(lse[:, heads, t].cpu().numpy().ravel(), rl, **TOL)
 
 
+def test_cfg5_128k_backward_rows_and_identities():
+    """cfg5 (S=128K, H=32) fwd+bwd: the dK/dV identities over every head and key,
+    and sampled dQ rows and dK/dV key rows of two heads against the oracle.  The
+    key rows sit in the last stripe period (a stripe key attended by every later
+    row, a local-only key, the last key), so the oracle's row sums stay short."""
+    torch = _torch()
+    cfg = s2.make_s2_config(131072, 32, block_size=64, local_blocks=4, vert_stride=16)
+    N, H, D, S = cfg.seq_len, cfg.num_heads, 128, cfg.block_size
+    B = cfg.num_blocks()
+    g = torch.Generator(device="cuda").manual_seed(37)
+    q, k, v, do = (_uniform((1, H, N, D), g) for _ in range(4))
+    plan = s2.Plan.from_config(cfg)
+    out, lse = s2.s2_attn_fwd(plan, q, k, v)
+    dq, dk, dv = s2.s2_attn_bwd(plan, q, k, v, out, lse, do)
+    torch.cuda.synchronize()
+    for h in range(H):  # sum_j dV_j = sum_i dO_i ; sum_j dK_j = 0, per head
+        sdv, sdo = dv[0, h].double().sum(0), do[0, h].double().sum(0)
+        assert torch.all((sdv - sdo).abs() <= 1e-3 * dv[0, h].double().abs().sum(0) + 1e-3), f"dV sum head {h}"
+        assert torch.all(dk[0, h].double().sum(0).abs() <= 1e-3 * dk[0, h].double().abs().sum(0) + 1e-3), \
+            f"dK sum head {h}"
+    heads = [5, 26]
+    rp, ci = oracle.csr_all(cfg)
+    srp, sci = _csr_heads(rp, ci, B, heads)
+    sel = lambda t: np.ascontiguousarray(_host(t[:, heads]).ravel())  # noqa: E731
+    hq, hk, hv, hdo = sel(q), sel(k), sel(v), sel(do)
+    q_rows = [(u, i) for u in range(2) for i in (0, 64, 65535, 100003, N - 1)]
+    k_rows = []
+    for u, h in enumerate(heads):
+        o = h % 16
+        sb = o + 16 * ((B - 8 - o) // 16)  # the last stripe block with >= 4 later blocks
+        k_rows += [(u, sb * S + 5), (u, (sb + 1) * S + 7), (u, N - 1)]
+    rq, rk, rv = oracle.bwd_sample(hq, hk, hv, hdo, srp, sci, 1, 2, 2, N, D, S, q_rows, k_rows)
+    gq, gk, gv = (_host(t[0, heads]) for t in (dq, dk, dv))
+    for n, (u, i) in enumerate(q_rows):
+        np.testing.assert_allclose(gq[u, i], rq[n], **TOL, err_msg=f"dq head {heads[u]} row {i}")
+    for n, (u, j) in enumerate(k_rows):
+        np.testing.assert_allclose(gk[u, j], rk[n], **TOL, err_msg=f"dk head {heads[u]} key {j}")
+        np.testing.assert_allclose(gv[u, j], rv[n], **TOL, err_msg=f"dv head {heads[u]} key {j}")
+
+
 def test_cfg4_decode_full_context_matches_oracle():
     torch = _torch()
     from paper_2407_17678_b200.decode import KVCache

@@ -27,7 +27,21 @@ def test_rng_stream_matches_reference_fixture():
     assert q.tolist() == r["q"] and k.tolist() == r["k"] and v.tolist() == r["v"]
 
 
-@pytest.mark.parametrize("name", [k for k in LAYOUTS if LAYOUTS[k]["config"]["seq_len"] <= 32768])
+def test_product_random_tensors_is_the_reference_stream():
+    """The Python mirror's AttentionTensors.random (s2_random_tensors in the
+    library) reproduces the reference's mt19937_64 stream: the fixture made by
+    the reference, and the port at a larger size."""
+    import paper_2407_17678_b200 as s2
+
+    r = FWD["rng"]
+    t = s2.AttentionTensors.random(r["H"], r["N"], r["d"], r["seed"])
+    assert t.q.tolist() == r["q"] and t.k.tolist() == r["k"] and t.v.tolist() == r["v"]
+    t = s2.AttentionTensors.random(8, 2048, 64, 7)  # cfg1 with bench_attention.cpp:34's seed
+    q, k, v = oracle.random_tensors(8, 2048, 64, 7)
+    assert np.array_equal(t.q, q) and np.array_equal(t.k, k) and np.array_equal(t.v, v)
+
+
+@pytest.mark.parametrize("name", list(LAYOUTS))
 def test_port_layout_matches_reference_fixture(name):
     rec = LAYOUTS[name]
     cfg = cfg_from_dict(rec["config"])
