@@ -35,3 +35,18 @@ def test_reference_arm_prints_one_line_with_its_thread_count():
     cores = len(os.sched_getaffinity(0))
     assert d["cpu_baseline"]["cores"] == cores and f"{cores} threads" in d["cpu_baseline"]["sample"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_reference_arm_loads_nothing_from_the_product():
+    """The reference arm runs the reference library and the oracle only: neither the
+    product package nor its libraries are imported or mapped."""
+    code = (
+        "import sys, argparse; sys.path.insert(0, %r); import bench; "
+        "bench.run_reference(argparse.Namespace(gpus=1, steps=1, warmup=0)); "
+        "maps = open('/proc/self/maps').read(); "
+        "print('PRODUCT', any(m.startswith('paper_2407_17678_b200') for m in sys.modules), "
+        "'libs2attn' in maps, 'libshardattn_b200' in maps)" % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    last = [ln for ln in r.stdout.splitlines() if ln.startswith("PRODUCT")][-1]
+    assert last == "PRODUCT False False False", last

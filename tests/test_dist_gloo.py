@@ -108,3 +108,23 @@ def test_head_parallel_world2_gloo_matches_single_process(case, tmp_path):
     # both ranks got work and LPT balanced it
     assert set(r["owner"].tolist()) == {0, 1}
     assert r["load"].max() <= r["load"].sum() / 2 * 1.5
+
+
+def test_cfg5_shaped_split_32_heads_over_8_ranks_gloo(tmp_path):
+    """bench.py --workload cfg5's split at world 8: one sequence's 32 heads
+    (heterogeneous offsets) LPT-assigned by active blocks, 4 per rank, gathered
+    output bit-identical to one process (small N: the oracle computes locally)."""
+    import torch.multiprocessing as mp
+
+    import oracle
+
+    cfg, batch, D = single(1024, 64, 32, 4, 16), 1, 8
+    res = str(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(8, _free_port(), cfg, batch, D, res), nprocs=8, join=True)
+    r = np.load(res)
+    rp, ci = oracle.csr_all(cfg)
+    ro, rl = oracle.attn_fwd(r["q"].ravel(), r["k"].ravel(), r["v"].ravel(), rp, ci, batch, 32, 32, 1024, D, 64)
+    np.testing.assert_array_equal(r["out"].ravel(), ro)
+    np.testing.assert_array_equal(r["lse"].ravel(), rl.astype(np.float32))
+    assert sorted(np.bincount(r["owner"], minlength=8).tolist()) == [4] * 8
+    assert r["load"].max() / (r["load"].sum() / 8) < 1.05

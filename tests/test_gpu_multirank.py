@@ -106,6 +106,25 @@ def test_bench_world2_prints_one_valid_line(exchange):
     assert ("fused" in d["config"]["parallelism"]) == (exchange == "fused")
 
 
+def test_bench_cfg5_strong_world2_prints_one_valid_line():
+    """--workload cfg5: the 128K layer's 32 heads split over 2 ranks (strong scaling),
+    with the exchange budget in the line."""
+    env = dict(os.environ, S2_BENCH_SHARE_GPU="1", S2_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--workload", "cfg5", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-3000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["seq_len"] == 131072 and d["config"]["global_batch"] == 1
+    ex = d["exchange"]
+    assert len(ex["rank_active_blocks"]) == 2 and ex["imbalance_max_over_ideal"] < 1.01
+    assert ex["all_gather_bytes_total"] == 32 * 131072 * 128 * 2
+
+
 def _fused_worker(rank, world, port, cfg, batch, D, res_dir):
     import torch
     import torch.distributed as dist
