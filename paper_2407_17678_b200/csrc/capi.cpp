@@ -20,6 +20,11 @@ cudaError_t s2_launch_fwd_sm100(int head_dim, const CUtensorMap& q, const CUtens
                                 int seq_len, int hpg, float scale_log2, cudaStream_t stream,
                                 int num_peers, const int* unit_global, float* const* peer_lse,
                                 const CUtensorMap* peer_o);
+int s2_fwd_pair2_clusters();
+cudaError_t s2_launch_fwd_pair2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                                const CUtensorMap& o, const void* items, const int* sched, int clusters,
+                                const void* steps, float* lse, int seq_len, int hpg, float scale_log2,
+                                cudaStream_t stream);
 cudaError_t s2_launch_fwd_simt(bool bf16, const void* q, const void* k, const void* v, void* out,
                                float* lse, const int* bh_list, const int* head_of, int num_bh,
                                const int* row_ptr, const int* col_idx, const int64_t* col_off,
@@ -186,6 +191,13 @@ static std::vector<int32_t> schedule_items(std::vector<T>& items, int grid, Cost
     return off;
 }
 
+// The CTA-pair forward (fwd_pair2.cu) serves head_dim 128 when S2_FWD_2CTA=1
+// (opt-in until it beats the 1-CTA pair kernel on cfg3).
+static bool pair2_enabled() {
+    const char* e = getenv("S2_FWD_2CTA");
+    return e && e[0] == '1';
+}
+
 static int dkv_group() {
     const char* e = getenv("S2_DKV_GROUP");
     return e ? atoi(e) : 0;
@@ -205,7 +217,8 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
     // the forward fills every SM; the backward kernels leave s2_set_sm_reserve SMs
     // to the collective that overlaps them (the all-gather of O)
     const int grid_fwd = num_sms(), grid = persistent_grid();
-    std::string key = std::to_string(batch) + ":g" + std::to_string(grid_fwd) + "/" + std::to_string(grid) + ":";
+    std::string key = std::to_string(batch) + ":g" + std::to_string(grid_fwd) + "/" + std::to_string(grid) +
+                      (pair2_enabled() ? "p2" : "") + ":";
     std::vector<int> units;
     if (unit_ids) {
         units.assign(unit_ids, unit_ids + num_units);
@@ -264,6 +277,22 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
                 pi.push_back({bh[i], q, static_cast<int32_t>(L->pairs.offset[w_ + 1] - off),
                               2 * q + 1 < nt ? 1 : 0, off});
             }
+        // CTA-pair forward: both tiles of a pair are computed whatever their masks
+        std::vector<PairItem> pi2;
+        const int clusters = pair2_enabled() ? s2_fwd_pair2_clusters() : 0;
+        if (clusters > 0) {
+            pi2 = pi;
+            const std::vector<int32_t> off2 = schedule_items(
+                pi2, clusters, [](const PairItem& a) { return int64_t(a.nsteps) * 2; },
+                [](const PairItem& a) { return a.bh; }, sched_overhead("S2_SCHED_OVH_FWD2", 3));
+            w->clusters = clusters;
+            w->num_pair2 = static_cast<int>(pi2.size());
+            if ((e = upload(w->pair2, pi2.data(), pi2.size() * sizeof(PairItem))) != cudaSuccess ||
+                (e = upload(w->pair2_sched, off2.data(), off2.size() * sizeof(int32_t))) != cudaSuccess) {
+                *status = cuda_fail(e, "uploading work items");
+                return nullptr;
+            }
+        }
         const std::vector<int32_t> off_pair = schedule_items(
             pi, grid_fwd, [](const PairItem& a) { return int64_t(a.nsteps) * (1 + a.has_b); },
             [](const PairItem& a) { return a.bh; }, sched_overhead("S2_SCHED_OVH_FWD", 4));
@@ -726,6 +755,15 @@ static int attn_fwd_impl(s2_plan* p, const s2_attn_args* a, int num_peers, void*
             CUtensorMap peer_maps[8];
             for (int r = 0; r < num_peers; ++r)
                 peer_maps[r] = s2host::make_map_bf16_3d(peer_out[r], D, N, uint64_t(total_units) * hpg, 64, 128);
+            if (num_peers == 0 && D == 128 && w->clusters > 0) {
+                // CTA pairs: V as 64-column boxes (each CTA holds its D half of a chunk)
+                const CUtensorMap mv2 = s2host::make_map_bf16_3d(a->v, D, N, nu, 64, 64);
+                ProfScope prof("fwd_sm100", st);
+                e = s2_launch_fwd_pair2(mq, mk, mv2, mo, w->pair2.ptr, w->pair2_sched.as<int>(), w->clusters,
+                                        L->d_steps.ptr, a->lse, a->seq_len, hpg, float(scale * M_LOG2E), st);
+                if (e != cudaSuccess) return cuda_fail(e, "s2_attn_fwd launch");
+                return S2_OK;
+            }
             ProfScope prof("fwd_sm100", st);
             e = s2_launch_fwd_sm100(a->head_dim, mq, mk, mv, mo, w->pair.ptr, w->pair_sched.as<int>(),
                                     w->grid_fwd, L->d_steps.ptr, static_cast<__nv_bfloat16*>(a->out),

@@ -34,6 +34,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "fwd_mask.cuh"
 #include "sm100_ptx.cuh"
 
 namespace s2dev {
@@ -111,22 +112,6 @@ struct Fwd2Cfg {
     static constexpr int kStgBytes = 16384;
     static constexpr int kSmem = 1024 + 2 * kQBytes + kNST * kStageBytes + 2 * kStgBytes;
 };
-
-__device__ __forceinline__ void apply_mask(float* s, int chunk, uint32_t mask, int rg, int q_pos,
-                                           int qtile_row0) {
-    const uint32_t bits = (mask >> (rg * 4)) & 0xFu;
-    const int key0 = chunk * 64;
-    const bool diag = key0 + 63 > qtile_row0;
-    if (bits == 0xFu && !diag) return;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-        const bool on = (bits >> g) & 1u;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if (!on || (diag && key0 + g * 16 + j > q_pos)) s[g * 16 + j] = -INFINITY;
-        }
-    }
-}
 
 template <int D, bool PEERS>
 __global__ void __launch_bounds__(384, 1)

@@ -45,7 +45,10 @@ struct WorkItems {
     DevBuf bwd;       // s2dev::BwdItem[]
     int num_bwd = 0;
     bool bwd_dropped = false;  // key tiles nobody attends (user CSR without diagonal): dK/dV = 0
-    DevBuf fwd_sched, pair_sched, bwd_sched;  // int[grid + 1] per-CTA item ranges
+    DevBuf pair2;     // PairItem[] regrouped for the CTA-pair forward (fwd_pair2.cu)
+    int num_pair2 = 0;
+    int clusters = 0;  // CTA pairs of the pair2 forward's persistent grid (0: not built)
+    DevBuf fwd_sched, pair_sched, bwd_sched, pair2_sched;  // int[grid + 1] per-CTA (per-cluster) item ranges
     int grid = 0;      // backward kernels (dQ: fwd_sched, dK/dV: bwd_sched): SMs minus the reserve
     int grid_fwd = 0;  // forward (pair_sched): every SM
     DevBuf simt_bh;   // int[num_bh] data index

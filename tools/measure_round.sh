@@ -11,15 +11,15 @@ timeout 600 python bench.py --steps 30 --warmup 5 > gpurun_out/bench_$TAG.json 2
 echo "bench rc=$?"; tail -c 600 gpurun_out/bench_$TAG.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-e2e \
-  --no-cpu-baseline --no-hybrid --no-decode > gpurun_out/ncu_launch_$TAG.log 2>&1
+  --no-cpu-baseline --no-hybrid --no-decode --no-configs > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo "launches rc=$?"
 timeout 600 python tests/selftest.py --csv gpurun_out/selftest_$TAG.csv > gpurun_out/selftest_$TAG.log 2>&1
 echo "selftest rc=$?"; tail -2 gpurun_out/selftest_$TAG.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'s2_(fwd_sm100|bwd)' -c 4 \
-  -o gpurun_out/bwd_full_$TAG -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \
+  -o gpurun_out/bwd_full_$TAG -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-configs \
   --no-hybrid --no-decode > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "ncu full rc=$?"
 timeout 600 ncu --set full --clock-control none -k regex:'s2_decode_split' -c 1 \
-  -o gpurun_out/dec_full_$TAG -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \
+  -o gpurun_out/dec_full_$TAG -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-configs \
   --no-hybrid > gpurun_out/ncu_dec_$TAG.log 2>&1
 echo "ncu dec rc=$?"
