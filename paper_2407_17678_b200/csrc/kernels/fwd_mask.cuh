@@ -25,4 +25,21 @@ __device__ __forceinline__ void apply_mask(float* s, int chunk, uint32_t mask, i
     }
 }
 
+// The same rule for 32 of the chunk's 64 columns: piece `half` (columns
+// [32 half, 32 half + 32), groups 2 half and 2 half + 1).
+__device__ __forceinline__ void apply_mask32(float* s, int chunk, uint32_t mask, int rg, int q_pos, int qtile_row0,
+                                             int half) {
+    const uint32_t bits = (mask >> (rg * 4 + 2 * half)) & 0x3u;
+    const int key0 = chunk * 64 + 32 * half;
+    const bool diag = chunk * 64 + 63 > qtile_row0;
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        const bool on = (bits >> g) & 1u;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (!on || (diag && key0 + g * 16 + j > q_pos)) s[g * 16 + j] = -INFINITY;
+        }
+    }
+}
+
 }  // namespace s2dev

@@ -29,11 +29,15 @@ print(f"S issuer: wait K {m(t[1, lo:hi] - t[0, lo:hi]):.0f}, wait buffer (P V k-
       f"issue -> next {m(t[0, lo + 1:hi + 1] - t[2, lo:hi]):.0f}, period {m(np.diff(t[0, lo:hi])):.0f}")
 print(f"PV issuer: wait P {m(t[4, lo:hi] - t[3, lo:hi]):.0f}, issue -> next {m(t[3, lo + 1:hi + 1] - t[11, lo:hi]):.0f}, "
       f"period {m(np.diff(t[3, lo:hi])):.0f}")
+ns = int((t[6] > 0).sum())  # softmax rows are indexed per warpgroup step when the warpgroups alternate steps
+slo, shi = (lo, hi) if ns > n * 3 // 4 else (5, ns - 2)
 for rk, X in ((0, 0), (0, 1), (1, 0), (1, 1)):
     o = 24 * rk + 12 * X
+    lo, hi = slo, shi
     print(f"softmax rank {rk} wg {X}: wait S {m(t[o + 6, lo:hi] - t[o + 5, lo:hi]):.0f}, ld+mask+max {m(t[o + 7, lo:hi] - t[o + 6, lo:hi]):.0f}, "
           f"exp+store+arrive {m(t[o + 8, lo:hi] - t[o + 7, lo:hi]):.0f}, arrive -> next wait {m(t[o + 5, lo + 1:hi + 1] - t[o + 8, lo:hi]):.0f}, "
           f"period {m(np.diff(t[o + 6, lo:hi])):.0f}")
+lo, hi = 10, n - 2
 for rk in (0, 1):
     o = 24 * rk
     print(f"producer rank {rk}: wait stage {m(t[o + 10, lo:hi] - t[o + 9, lo:hi]):.0f}, period {m(np.diff(t[o + 9, lo:hi])):.0f}")
