@@ -709,9 +709,17 @@ def bench_configs(s2, args, dev, lib, pk, pk_kind, with_cpu):
         out, lse = s2.s2_attn_fwd(plan, q, k, v)
         ms = _time_steps(lambda: s2.s2_attn_fwd(plan, q, k, v, out=out, lse=lse), 20, 3)
         act, _ = plan.fwd_flops(1, 64)
+        pk_, _src = peaks()
+        mhz = float(pk_.get("sm_max_mhz", 1965.0))
+        fp32_peak = 148 * 128 * 2 * mhz * 1e6 / 1e12  # FFMA lanes x 2 flops x clock
+        ach = act / (ms * 1e-3) / 1e12
         r = {"workload": "cfg1: fp32 forward B=1 H=8 S=2048 D=64, block 64, local 4, vert_stride 8",
-             "dtype": "f32", "ms": ms, "tflops_active": act / (ms * 1e-3) / 1e12,
-             "kernel": "s2_fwd_simt_kernel (fp32 FFMA, the 1e-4 parity path)"}
+             "dtype": "f32", "ms": ms, "tflops_active": ach,
+             "kernel": "s2_fwd_tile_kernel (fp32 FFMA from shared-memory tiles, the 1e-4 parity path)",
+             "roofline": {"bound": "fp32 FFMA (SIMT)", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                          "frac": ach / fp32_peak, "traffic": None,
+                          "peak_source": "derived: 148 SMs x 128 FFMA/clk x 2 x sm_max_mhz (not measured)",
+                          "alg_flops_per_launch": act}}
         if with_cpu:
             cb = reference_cfg1_full()
             r["cpu_baseline"] = cb

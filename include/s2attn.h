@@ -168,8 +168,10 @@ int s2_plan_head_nnz(const s2_plan* plan, int head, int64_t* nnz);
  * (test_attention.cpp:124-132).
  *
  * Kernels: bf16 with head_dim 64 / 128 and block_size % 16 == 0 runs the
- * tcgen05 kernel; every other bf16 / fp32 case with head_dim <= 2048 runs the
- * SIMT kernel; head_dim > 2048 fails with S2_ERR_UNSUPPORTED.
+ * tcgen05 kernel (the only shapes s2_attn_bwd supports); every other bf16 /
+ * fp32 case runs an fp32-FFMA kernel -- shared-memory tiles for
+ * head_dim <= 256, one warp per row up to 2048 -- with no tensor cores and no
+ * backward (S2_ERR_UNSUPPORTED); head_dim > 2048 fails with S2_ERR_UNSUPPORTED.
  *
  * Units: the head-parallel partitioner works on (batch, kv-group) units,
  * u = b*num_kv_heads + g.  unit_ids == NULL processes every unit and the

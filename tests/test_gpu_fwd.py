@@ -256,6 +256,26 @@ def test_f32_any_head_dim_matches_oracle(d):
     np.testing.assert_allclose(t.lse, rl, **F32_TOL)
 
 
+@pytest.mark.parametrize("N,S,d,rowwise", [(1000, 128, 64, False), (333, 8, 40, False), (777, 96, 128, False),
+                                           (1000, 128, 64, True), (520, 64, 256, False), (65, 200, 17, False)])
+def test_f32_tiled_kernel_blocks_and_tails(N, S, d, rowwise, monkeypatch):
+    """The tiled fp32 kernel's 64-row sub-tiles of large blocks (S=128, 200), small
+    blocks (S=8), ragged N and head dims that are not multiples of 4 -- and the same
+    case on the row-wise kernel (S2_SIMT_ROWWISE=1) -- vs the oracle at 1e-4."""
+    if rowwise:
+        monkeypatch.setenv("S2_SIMT_ROWWISE", "1")
+    cfg = s2.make_single_stride_config(N, S, 2, 2, 3)
+    H = 2
+    q, k, v = oracle.random_tensors(H, N, d, 7 + d + S)
+    t = s2.AttentionTensors.zeros(H, N, d)
+    t.q, t.k, t.v = q, k, v
+    s2.streaming_sharded_attention(t, s2.build_all_csr(cfg), S)
+    rp, ci = oracle.csr_all(cfg)
+    ro, rl = oracle.attn_fwd(q, k, v, rp, ci, 1, H, H, N, d, S)
+    np.testing.assert_allclose(t.out, ro, **F32_TOL)
+    np.testing.assert_allclose(t.lse, rl, **F32_TOL)
+
+
 @pytest.mark.parametrize("d", [32, 96, 256])
 def test_bf16_other_head_dims_take_the_simt_kernel_and_match_oracle(d):
     """bf16 with a head dim the tensor-core kernel does not take (not 64 / 128) runs
@@ -274,3 +294,6 @@ def test_bf16_other_head_dims_take_the_simt_kernel_and_match_oracle(d):
     ro, rl = oracle.attn_fwd(q, k, v, rp, ci, 1, H, Hkv, N, d, S)
     np.testing.assert_allclose(out.float().cpu().numpy().ravel(), ro, rtol=1e-2, atol=1e-2)
     np.testing.assert_allclose(lse.cpu().numpy().ravel(), rl, rtol=1e-2, atol=1e-2)
+    # no backward for these shapes: an explicit error, never a silent fallback
+    with pytest.raises(s2.S2Unsupported):
+        s2.s2_attn_bwd(s2.Plan.from_config(cfg), T(q, H), T(k, Hkv), T(v, Hkv), out, lse, out)

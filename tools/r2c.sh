@@ -1,2 +1,1 @@
-export S2_FWD_2CTA=1
-timeout 120 python tools/trace_fwd2.py 2>&1 | tail -16
+timeout 900 python -m pytest tests/test_gpu_fwd.py tests/test_gpu_selftest.py -m gpu -q -x -p no:cacheprovider 2>&1 | tail -3
