@@ -366,9 +366,11 @@ def _kernel_profile(lib, fn, steps, barrier):
     return kernels
 
 
-def _roofline(kernels, fwd_flops, pk, pk_kind):
+def _roofline(kernels, fwd_flops, pk, pk_kind, with_traffic=True):
     """Roofline of the dominant kernel; algorithmic FLOPs per launch:
-    fwd_sm100: F; bwd_dkv: S-recompute + dP + dV + dK = 2F; bwd_dq: dQ = 0.5F."""
+    fwd_sm100: F; bwd_dkv: S-recompute + dP + dV + dK = 2F; bwd_dq: dQ = 0.5F.
+    traffic: the committed ncu capture is of the cfg3 workload only, so other
+    workloads report null (with_traffic=False)."""
     alg = {"fwd_sm100": fwd_flops, "bwd_dkv_sm100": 2.0 * fwd_flops, "bwd_dq_sm100": 0.5 * fwd_flops,
            "bwd_prep": 0.0}
     dom = max(kernels, key=lambda k_: kernels[k_]["avg_ms"]) if kernels else None
@@ -376,8 +378,10 @@ def _roofline(kernels, fwd_flops, pk, pk_kind):
         return None
     ach = alg.get(dom, 0.0) / (kernels[dom]["avg_ms"] * 1e-3) / 1e12
     return {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"],
-            "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops"], "traffic": ncu_traffic(dom),
-            "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read+write per launch, ncu --set full)",
+            "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops"],
+            "traffic": ncu_traffic(dom) if with_traffic else None,
+            "traffic_source": ("profiles/ncu_traffic.json (dram__bytes_read+write per launch, ncu --set full, cfg3)"
+                               if with_traffic else "no ncu capture of this workload"),
             "peak_source": f"{pk_kind} bf16_tflops (burst)",
             "frac_of_sustained": ach / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
             "alg_flops_per_launch": alg.get(dom, 0.0)}
@@ -505,7 +509,7 @@ def run_s2(args):
     fwd_ms = kernels.get("fwd_sm100", {}).get("avg_ms", float("nan"))
     bwd_ms = sum(kernels.get(k_, {}).get("avg_ms", 0.0) for k_ in ("bwd_prep", "bwd_dkv_sm100", "bwd_dq_sm100"))
     pk, pk_kind = peaks()
-    roof = _roofline(kernels, my_fwd_flops, pk, pk_kind)
+    roof = _roofline(kernels, my_fwd_flops, pk, pk_kind, with_traffic=args.workload == "cfg3")
 
     if cfg5:
         cdesc = {"workload": "cfg5: one S2 attention layer fwd+bwd, S=131072, H=32, D=128, B=1, block 64, "
@@ -748,7 +752,7 @@ def bench_configs(s2, args, dev, lib, pk, pk_kind, with_cpu):
             r = {"workload": f"{name}: bf16 fwd+bwd B={B_} H=32 S={N_} D=128, block 64, local 4, vert_stride 16",
                  "dtype": "bf16", "ms_per_step": ms, "tflops_active": 3.5 * act / (ms * 1e-3) / 1e12,
                  "dense_equiv_tflops": 3.5 * dense / (ms * 1e-3) / 1e12, "kernels": kern,
-                 "roofline": _roofline(kern, act, pk, pk_kind)}
+                 "roofline": _roofline(kern, act, pk, pk_kind, with_traffic=False)}
             if with_cpu:
                 v_, s_, kind, desc, _ = cpu_sample(seq_len=N_, heads=(0,), band=1.0 if N_ <= 8192 else 0.125)
                 r["cpu_baseline"] = {"value": v_, "unit": "TFLOP/s", "cores": use_all_host_threads(), "kind": kind,
