@@ -13,7 +13,8 @@ cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CU
                                 const CUtensorMap& o1, const void* items, const int* sched, int grid,
                                 const void* entries, const float* lse2, const float* delta,
                                 int N, int Npad, int hpg, float scale, cudaStream_t stream,
-                                void* g0, void* g1);
+                                void* g0, void* g1, const void* fused_o = nullptr,
+                                const void* fused_dout = nullptr, const float* fused_lse = nullptr);
 
 using namespace s2;
 
@@ -67,8 +68,18 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
     const double scale = resolve_scale(f.scale, D);
     float* delta = static_cast<float*>(workspace);
     float* lse2 = delta + static_cast<size_t>(nqbh) * Npad;
-    cudaError_t e;
-    {
+    cudaError_t e = cudaSuccess;
+    // S2_PREP_FUSED=1 fuses the prep (Delta = rowsum(dO o O), lse2) into the dQ
+    // kernel, which then runs first and leaves both in the workspace for dK/dV.  Off
+    // by default: the per-item row loads of O and dO stall the elementwise warps at
+    // item starts (cfg3: dQ 0.83 -> 1.06 ms against the 0.10 ms prep it saves).
+    const char* dkv_env = std::getenv("S2_DKV_V2");
+    const bool dkv_v1 = !(dkv_env && dkv_env[0] == '1');
+    const char* dq_env = std::getenv("S2_DQ_V2");
+    const bool dq_v1 = !(dq_env && dq_env[0] == '1');
+    const char* fz_env = std::getenv("S2_PREP_FUSED");
+    const bool fused = dq_v1 && fz_env && fz_env[0] == '1';
+    if (!fused) {
         ProfScope prof("bwd_prep", st);
         e = s2_launch_bwd_prep(static_cast<const __nv_bfloat16*>(f.out),
                                static_cast<const __nv_bfloat16*>(a->dout), f.lse, delta, lse2,
@@ -100,30 +111,33 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
         const CUtensorMap mdk = make_map_bf16_3d(a->dk, D, N, nkv, 64, 64);
         const CUtensorMap mdv = make_map_bf16_3d(a->dv, D, N, nkv, 64, 64);
         const CUtensorMap mdq = make_map_bf16_3d(a->dq, D, N, nqbh, 64, 128);
-        {
-            ProfScope prof("bwd_dkv_sm100", st);
-            // S2_DKV_V2=1: the experimental 128-row-step dK/dV kernel (s2_bwd_dkv2_kernel;
-            // slower at cfg3, DESIGN.md section 4)
-            const char* dkv_env = std::getenv("S2_DKV_V2");
-            const bool dkv_v1 = !(dkv_env && dkv_env[0] == '1');
-            if (dkv_v1)
-                e = s2_launch_bwd_sm100(0, D, q64, do64, mk, mv, mdk, mdv, w->bwd.ptr, w->bwd_sched.as<int>(),
-                                        w->grid, L->d_entries.ptr, lse2, delta, N, Npad, hpg, float(scale), st,
-                                        nullptr, nullptr);
-            else
-                e = s2_launch_bwd_sm100(3, D, q128, do128, mk, mv, mdk, mdv, w->bwd.ptr, w->bwd_sched.as<int>(),
-                                        w->grid, L->d_entries.ptr, lse2, delta, N, Npad, hpg, float(scale), st,
-                                        a->dk, a->dv);
-        }
-        if (e == cudaSuccess) {
+        auto run_dq = [&]() {
             ProfScope prof("bwd_dq_sm100", st);
             // S2_DQ_V2=1: the experimental 128-key-step dQ kernel (s2_bwd_dq2_kernel;
             // slower at cfg3: its two-chunk K/V stages need 8 KB TMA boxes)
-            const char* dq_env = std::getenv("S2_DQ_V2");
-            const bool dq_v1 = !(dq_env && dq_env[0] == '1');
-            e = s2_launch_bwd_sm100(dq_v1 ? 1 : 2, D, q128, do128, dq_v1 ? mk4 : mk, dq_v1 ? mv4 : mv, mdq, mdq, w->fwd.ptr, w->fwd_sched.as<int>(),
-                                    w->grid, L->d_chunks.ptr, lse2, delta, N, Npad, hpg, float(scale), st,
-                                    nullptr, nullptr);
+            return s2_launch_bwd_sm100(dq_v1 ? 1 : 2, D, q128, do128, dq_v1 ? mk4 : mk, dq_v1 ? mv4 : mv, mdq, mdq,
+                                       w->fwd.ptr, w->fwd_sched.as<int>(), w->grid, L->d_chunks.ptr, lse2, delta, N,
+                                       Npad, hpg, float(scale), st, nullptr, nullptr, fused ? f.out : nullptr,
+                                       a->dout, f.lse);
+        };
+        auto run_dkv = [&]() {
+            ProfScope prof("bwd_dkv_sm100", st);
+            // S2_DKV_V2=1: the experimental 128-row-step dK/dV kernel (s2_bwd_dkv2_kernel;
+            // slower at cfg3, DESIGN.md section 4)
+            if (dkv_v1)
+                return s2_launch_bwd_sm100(0, D, q64, do64, mk, mv, mdk, mdv, w->bwd.ptr, w->bwd_sched.as<int>(),
+                                           w->grid, L->d_entries.ptr, lse2, delta, N, Npad, hpg, float(scale), st,
+                                           nullptr, nullptr);
+            return s2_launch_bwd_sm100(3, D, q128, do128, mk, mv, mdk, mdv, w->bwd.ptr, w->bwd_sched.as<int>(),
+                                       w->grid, L->d_entries.ptr, lse2, delta, N, Npad, hpg, float(scale), st,
+                                       a->dk, a->dv);
+        };
+        if (fused) {
+            e = run_dq();
+            if (e == cudaSuccess) e = run_dkv();
+        } else {
+            e = run_dkv();
+            if (e == cudaSuccess) e = run_dq();
         }
     } catch (const std::exception& ex) {
         return fail(S2_ERR_CUDA, ex.what());

@@ -104,6 +104,12 @@ struct BwdParams {
     float scale_log2, scale;
     long long* trace;  // debug: per-step clock64 of CTA 0 (nullptr = off)
     int debug;         // debug ablations (0 in production)
+    // dQ kernel with the prep fused (s2_bwd_dq_kernel only): it computes Delta and
+    // lse2 of its tile's rows from O, dO and lse and writes them to the workspace
+    // rows (lse2 / delta above) that the dK/dV kernel, launched after it, reads
+    const __nv_bfloat16* o;    // nullptr: not fused (the prep kernel ran)
+    const __nv_bfloat16* dout;
+    const float* lse;          // the forward's lse (natural log) [num_qbh][N]
 };
 
 #define S2TRACE(slot, n)                                                       \
@@ -140,7 +146,7 @@ struct BwdCfg {
 #endif
     static constexpr int kNSTq = S2_DQ_NST;
     static constexpr int kDqStage = 2 * kTile64;
-    static constexpr int kDqBars = 256;
+    static constexpr int kDqBars = 256 + 1024;  // barriers | fused prep: 2 x 128 partial row dots
     static constexpr int kDqSmem = 3 * kTile128 + kNSTq * kDqStage + kDqBars;
 };
 
@@ -575,7 +581,7 @@ __global__ void __launch_bounds__(384, 1)
         uint64_t qf, qe, sf[NST], se[NST], s[2], p[2], af, ae;
         uint32_t tmem_base;
     };
-    static_assert(sizeof(Bars) <= C::kDqBars, "barrier block");
+    static_assert(sizeof(Bars) <= 256, "barrier block");
     Bars& bars = *reinterpret_cast<Bars*>(smem + 3 * C::kTile128 + NST * C::kDqStage);
     auto& bar_qf = bars.qf;
     auto& bar_qe = bars.qe;
@@ -739,8 +745,45 @@ __global__ void __launch_bounds__(384, 1)
             const FwdItem it = items[i];
             const int q_pos = it.qtile * 128 + r;
             const size_t lrow = static_cast<size_t>(it.bh) * p.Npad + q_pos;
-            const float l2 = p.lse2[lrow];
-            const float dl = p.delta[lrow];
+            float l2, dl;
+            if (p.o) {
+                // fused prep (s2_bwd_prep_kernel's rule): Delta = rowsum(dO o O) over
+                // this warpgroup's D/2 columns, the halves combined through shared
+                // memory; rows past seq_len and rows without an admitted key get
+                // lse2 = +inf, Delta = 0 (P = 0, dS finite)
+                float* part = reinterpret_cast<float*>(smem + 3 * C::kTile128 + NST * C::kDqStage + 256);
+                float acc = 0.f, l = -INFINITY;
+                if (q_pos < p.N) {
+                    const size_t off = (static_cast<size_t>(it.bh) * p.N + q_pos) * D + wg * (D / 2);
+                    const uint4* a4 = reinterpret_cast<const uint4*>(p.o + off);
+                    const uint4* b4 = reinterpret_cast<const uint4*>(p.dout + off);
+#pragma unroll
+                    for (int c = 0; c < D / 16; ++c) {
+                        const uint4 a = __ldg(a4 + c), b = __ldg(b4 + c);
+                        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+                        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float2 x = __bfloat1622float2(a2[j]), y = __bfloat1622float2(b2[j]);
+                            acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+                        }
+                    }
+                    l = p.lse[static_cast<size_t>(it.bh) * p.N + q_pos];
+                }
+                part[wg * 128 + r] = acc;
+                named_bar_sync(1, 256);
+                const float dot = part[r] + part[128 + r];
+                const bool live = l > -INFINITY;
+                dl = live ? dot : 0.f;
+                l2 = live ? l * 1.4426950408889634f : INFINITY;
+                if (wg == 0) {
+                    const_cast<float*>(p.delta)[lrow] = dl;
+                    const_cast<float*>(p.lse2)[lrow] = l2;
+                }
+            } else {
+                l2 = p.lse2[lrow];
+                dl = p.delta[lrow];
+            }
             const int rg = r >> 4;
             for (int n = 0; n < it.chunk_cnt; ++n, ++n_glob) {
                 const int2 ch = chunks[it.chunk_off + n];
@@ -1649,13 +1692,16 @@ cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CU
                                 const CUtensorMap& o1, const void* items, const int* sched, int grid,
                                 const void* entries, const float* lse2, const float* delta,
                                 int N, int Npad, int hpg, float scale, cudaStream_t stream,
-                                void* g0, void* g1) {
+                                void* g0, void* g1, const void* fused_o, const void* fused_dout,
+                                const float* fused_lse) {
     if (grid == 0) return cudaSuccess;
     const float sl2 = scale * 1.4426950408889634f;
     // debug bit 8 selects which kernel records the trace (0: dK/dV, 8: dQ)
     long long* tr = ((g_debug & 8) != 0) == (which == 1 || which == 2) ? g_trace : nullptr;
     BwdParams pp{items, sched, entries, lse2, delta, static_cast<__nv_bfloat16*>(g0), static_cast<__nv_bfloat16*>(g1),
-                 N, Npad, hpg, sl2, scale, tr, g_debug & ~8};
+                 N, Npad, hpg, sl2, scale, tr, g_debug & ~8,
+                 which == 1 ? static_cast<const __nv_bfloat16*>(fused_o) : nullptr,
+                 static_cast<const __nv_bfloat16*>(fused_dout), fused_lse};
     if (g_debug & 4) grid = 1;  // debug: isolate one CTA from memory-system contention
     if (which == 3) {  // dK/dV over 128-row q steps (q/do: 4-D 128-row maps; g0 = dK, g1 = dV)
         if (D == 128)

@@ -1,5 +1,6 @@
-"""The experimental 128-step backward kernels (S2_DKV_V2: dK/dV over 128-row q
-steps; S2_DQ_V2: dQ over 128-key steps), off by default because they are slower
+"""The experimental backward variants (S2_DKV_V2: dK/dV over 128-row q steps;
+S2_DQ_V2: dQ over 128-key steps; S2_PREP_FUSED: the prep fused into a dQ kernel
+that runs before dK/dV), off by default because they are slower
 at cfg3, against the oracle on the backward parity cases,
 so the code that stays in the library is checked like the default path."""
 import os
@@ -12,7 +13,7 @@ from test_gpu_bwd import CASES, TOL, run
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("env", ["S2_DKV_V2", "S2_DQ_V2"])
+@pytest.mark.parametrize("env", ["S2_DKV_V2", "S2_DQ_V2", "S2_PREP_FUSED"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_variant_matches_oracle(env, name):
     cfg, batch, D = CASES[name]
