@@ -1,2 +1,5 @@
-timeout 900 python -m pytest tests/test_gpu_bwd_variants.py tests/test_gpu_bwd.py -m gpu -q -x -p no:cacheprovider 2>&1 | tail -2
-for E in "S2_X=0" "S2_SCHED_OVH_FWD=0" "S2_SCHED_OVH_FWD=2" "S2_SCHED_OVH_FWD=8" "S2_SCHED_OVH_FWD=16" "S2_SCHED_OVH_DKV=0" "S2_SCHED_OVH_DKV=2" "S2_SCHED_OVH_DKV=8" "S2_SCHED_OVH_DKV=16" "S2_SCHED_OVH_DQ=0" "S2_SCHED_OVH_DQ=1" "S2_SCHED_OVH_DQ=4" "S2_SCHED_OVH_DQ=8" "S2_X=1"; do echo "== $E"; env $E timeout 120 python tools/perf_bwd.py --uniform 2>&1 | tail -1; done
+mkdir -p gpurun_out
+for tool in memcheck racecheck; do
+  S2_FWD_2CTA=1 timeout 900 compute-sanitizer --tool $tool python tools/sanitize_run.py > gpurun_out/san_${tool}.log 2>&1
+  echo "$tool rc=$?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|ok$" gpurun_out/san_${tool}.log | tail -12
+done

@@ -5,7 +5,8 @@
     compute-sanitizer --tool synccheck python tools/sanitize_run.py
 
 It covers the bf16 tcgen05 forward and backward (D = 64 / 128, MHA and GQA, a ragged
-N, batch 2, a tile with no keys), the fp32 SIMT forward, the layout / compaction /
+N, batch 2, a tile with no keys), the fp32 forwards (tiled and row-wise), the CTA-pair forward when S2_FWD_2CTA=1,
+the layout / compaction /
 append kernels and the split-KV decode with its combine.  Results are not checked here:
 the parity tests do that.  The process exits non-zero if a CUDA call fails.
 """
@@ -44,12 +45,21 @@ def main():
         torch.cuda.synchronize()
         print(f"bf16 fwd+bwd N={N} H={H}/{Hkv} D={D} batch={batch}: ok "
               f"(out {out.data_ptr():#x}+{out.nbytes}, dout {do.data_ptr():#x}+{do.nbytes})", flush=True)
-    # fp32 SIMT path
-    plan = s2.Plan.from_config(s2.make_s2_config(300, 2, block_size=32, local_blocks=2, vert_stride=2))
-    x = [rnd(1, 2, 300, 64, dt=torch.float32, g=g) for _ in range(3)]
-    s2.s2_attn_fwd(plan, *x)
-    torch.cuda.synchronize()
-    print("fp32 fwd: ok", flush=True)
+    # fp32 paths: the tiled kernel (block 32 and block 128 sub-tiles, D 64 / 17) and the
+    # row-wise kernel (D 300)
+    for N, S, D in ((300, 32, 64), (333, 128, 17), (200, 16, 300)):
+        plan = s2.Plan.from_config(s2.make_s2_config(N, 2, block_size=S, local_blocks=2, vert_stride=2))
+        x = [rnd(1, 2, N, D, dt=torch.float32, g=g) for _ in range(3)]
+        s2.s2_attn_fwd(plan, *x)
+        torch.cuda.synchronize()
+        print(f"fp32 fwd N={N} block={S} D={D}: ok", flush=True)
+    # the opt-in CTA-pair forward (fwd_pair2.cu)
+    if os.environ.get("S2_FWD_2CTA") == "1":
+        plan = s2.Plan.from_config(s2.make_s2_config(1000, 4, block_size=64, local_blocks=2, vert_stride=3))
+        q, k, vv = (rnd(1, 4, 1000, 128, g=g) for _ in range(3))
+        s2.s2_attn_fwd(plan, q, k, vv)
+        torch.cuda.synchronize()
+        print("pair2 fwd: ok", flush=True)
     # a row block without keys and an uncovered key block (zero-filled dK / dV)
     B = 8
     rows = [[0], [0, 1], [], [0, 3], [], [], [0, 6], [6, 7]]
