@@ -259,7 +259,7 @@ while time.monotonic() < end and not stop:
                                    nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
     except Exception:
         pass
-    time.sleep(0.0005)
+    time.sleep(float(sys.argv[3]))
     if len(buf) >= 200000:
         break
 sys.stdout.write("\n".join(buf) + "\n")
@@ -287,7 +287,8 @@ class ClockSampler:
             idx = self._nvml_index(pynvml, dev_index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(idx),
                                                             pynvml.NVML_CLOCK_SM)
-            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(idx), str(max_seconds)],
+            period = float(os.environ.get("S2_CLOCK_PERIOD_MS", "0.5")) * 1e-3
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(idx), str(max_seconds), str(period)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             if self.proc.stdout.readline().strip() != "ready":
                 self.proc = None

@@ -1244,6 +1244,18 @@ __global__ void __launch_bounds__(512, 1)
 // epilogue, 8-23 elementwise: four warpgroups (thread = key row = TMEM lane;
 // warpgroup w owns q columns [32w, 32w+32) of each step), so each SMSP holds
 // four elementwise warps to hide the exp / TMEM latencies of the others.
+#ifndef S2_DKV2_ALT
+#define S2_DKV2_ALT 0
+#endif
+// MMA issue: 2 = one issuer, dP^T-first order; 1 = two issuers (S^T / dP^T and
+// dV / dK); 0 = one issuer, S^T-first order
+#ifndef S2_DKV2_SPLIT
+#define S2_DKV2_SPLIT 2
+#endif
+// order 2 only: issue the previous step's dV / dK first when they are ready before S^T(g) is read
+#ifndef S2_DKV2_DYN
+#define S2_DKV2_DYN 0
+#endif
 template <int D>
 struct Dkv2Cfg {
     static constexpr int kSub = D / 64;
@@ -1268,7 +1280,7 @@ __global__ void __launch_bounds__(768, 1)
     if (tid == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1024-B alignment
     struct Bars {
         uint64_t kf, vf, kfree, vfree, qf[NQ], qe[NQ], of[NO], oe[NO], af[NA], ae[NA];
-        uint64_t sf, sfr, dpf, pds, accf, acce;
+        uint64_t sf, sfr, dpf, pds, accf, acce, rfree[2];
         uint4 meta[NA];  // per aux slot: first q row, chunk-0 / chunk-1 masks, query data index
         uint32_t tmem_base;
     };
@@ -1303,6 +1315,8 @@ __global__ void __launch_bounds__(768, 1)
         mbar_init(smem_u32(&bars.pds), 16);
         mbar_init(smem_u32(&bars.accf), 1);
         mbar_init(smem_u32(&bars.acce), 4);
+        mbar_init(smem_u32(&bars.rfree[0]), 1);
+        mbar_init(smem_u32(&bars.rfree[1]), 1);
         fence_mbar_init();
     }
     if (warp == 2) {
@@ -1374,7 +1388,230 @@ __global__ void __launch_bounds__(768, 1)
                     }
                 }
             }
-        } else if (warp == 1) {
+        } else if (warp == 1 && S2_DKV2_SPLIT == 1) {
+            // ---------------------------------------------- MMA issuer A: S^T, dP^T
+            // S^T(g) into region g & 1 once dV(g-2), dK(g-2) have read it (issuer B's
+            // rfree commit), dP^T(g) over it once the elementwise warps have read
+            // S^T(g).  With a second issuer for dV / dK, dP^T(g) is issued as soon as
+            // S^T(g) is read, while the exponentials of step g run (one issuer had
+            // to wait for step g-1's P / dS before it).
+            constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
+            const bool leader = elect_one();
+            const uint64_t dK0 = umma_desc_sw128(sK, 16, 1024), dV0 = umma_desc_sw128(sV, 16, 1024);
+            const uint64_t dQ0 = umma_desc_sw128(sQ0, 16, 1024), ddO0 = umma_desc_sw128(sdO0, 16, 1024);
+            uint32_t g = 0, ic = 0;
+            for (int i = i_beg; i < i_end; ++i) {
+                const int ns = warp_uniform(items[i].nsteps128);
+                if (ns == 0) continue;
+                for (int n = 0; n < ns; ++n) {
+                    const uint32_t gs = g + n;
+                    const uint32_t qs = gs % NQ;
+                    S2TRACE(0, gs);
+                    mbar_wait(smem_u32(&bars.qf[qs]), (gs / NQ) & 1);
+                    if (n == 0) mbar_wait(smem_u32(&bars.kf), ic & 1);
+                    if (gs >= 2) mbar_wait(smem_u32(&bars.rfree[gs & 1]), ((gs >> 1) - 1) & 1);
+                    S2TRACE(4, gs);
+                    tc_fence_after();
+                    if (leader) {
+                        const uint64_t b0 = dQ0 + static_cast<uint64_t>((qs * C::kT) >> 4);
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                            mma_ss(tmem + C::tR + 128 * (gs & 1), dK0 + o, b0 + o, idS, kk > 0);
+                        }
+                        mma_commit(smem_u32(&bars.sf));
+                        if (n == ns - 1) mma_commit(smem_u32(&bars.kfree));  // the item's K is read by S^T only
+                    }
+                    __syncwarp();
+                    S2TRACE(1, gs);
+                    // dP^T(gs) over S^T(gs) once the elementwise warps have read it
+                    const uint32_t os = gs % NO;
+                    mbar_wait(smem_u32(&bars.of[os]), (gs / NO) & 1);
+                    if (n == 0) mbar_wait(smem_u32(&bars.vf), ic & 1);
+                    mbar_wait(smem_u32(&bars.sfr), gs & 1);
+                    S2TRACE(13, gs);
+                    tc_fence_after();
+                    if (leader) {
+                        const uint64_t b0 = ddO0 + static_cast<uint64_t>((os * C::kT) >> 4);
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                            mma_ss(tmem + C::tR + 128 * (gs & 1), dV0 + o, b0 + o, idS, kk > 0);
+                        }
+                        mma_commit(smem_u32(&bars.dpf));
+                        if (n == ns - 1) mma_commit(smem_u32(&bars.vfree));  // V is read by dP^T only
+                    }
+                    __syncwarp();
+                    S2TRACE(14, gs);
+                }
+                g += ns;
+                ++ic;
+            }
+        } else if (warp == 3 && S2_DKV2_SPLIT == 1) {
+            // ---------------------------------------------- MMA issuer B: dV, dK
+            constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
+            const bool leader = elect_one();
+            const uint64_t dQmn = umma_desc_sw128(sQ0, 16384, 1024), ddOmn = umma_desc_sw128(sdO0, 16384, 1024);
+            uint32_t g = 0, ic = 0;
+            for (int i = i_beg; i < i_end; ++i) {
+                const int ns = warp_uniform(items[i].nsteps128);
+                if (ns == 0) continue;
+                for (int n = 0; n < ns; ++n, ++g) {
+                    mbar_wait(smem_u32(&bars.pds), g & 1);  // P^T(g), dS^T(g) in TMEM
+                    if (n == 0 && ic > 0) mbar_wait(smem_u32(&bars.acce), (ic - 1) & 1);
+                    S2TRACE(2, g);
+                    tc_fence_after();
+                    const uint32_t reg = C::tR + 128 * (g & 1);
+                    const uint32_t os = g % NO, qs = g % NQ;
+                    if (leader) {
+                        const uint64_t bo = ddOmn + static_cast<uint64_t>((os * C::kT) >> 4);
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk)  // K-dim: the step's 128 q rows; P^T at +16
+                            mma_ts(tmem + C::tdV, tmem + reg + (kk >> 1) * 32 + 16 + (kk & 1) * 8,
+                                   bo + ((kk * 2048) >> 4), idA, (n > 0 || kk > 0) ? 1u : 0u);
+                        mma_commit(smem_u32(&bars.oe[os]));  // dO(g) read (dP^T(g) complete earlier, dV(g))
+                        const uint64_t bq = dQmn + static_cast<uint64_t>((qs * C::kT) >> 4);
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk)  // dS^T at +0
+                            mma_ts(tmem + C::tdK, tmem + reg + (kk >> 1) * 32 + (kk & 1) * 8,
+                                   bq + ((kk * 2048) >> 4), idA, (n > 0 || kk > 0) ? 1u : 0u);
+                        mma_commit(smem_u32(&bars.qe[qs]));        // Q(g) read (S^T(g) complete earlier, dK(g))
+                        mma_commit(smem_u32(&bars.rfree[g & 1]));  // region g & 1 may take S^T(g+2)
+                        if (n == ns - 1) mma_commit(smem_u32(&bars.accf));
+                    }
+                    __syncwarp();
+                    S2TRACE(3, g);
+                }
+                ++ic;
+            }
+        } else if (warp == 1 && S2_DKV2_SPLIT == 2) {
+            // ---------------------------------- MMA issuer, dP^T-first order (default)
+            // Per step g:  dP^T(g) | dV(g-1) | dK(g-1) | S^T(g+1).  dP^T(g) goes to the
+            // pipe as soon as the elementwise warps have read S^T(g), ahead of the
+            // previous step's dV / dK, so it completes while they exponentiate; S^T(g+1)
+            // overwrites region (g+1)&1 right after dK(g-1) read it (in-order pipe).
+            constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
+            constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
+            const bool leader = elect_one();
+            const uint64_t dK0 = umma_desc_sw128(sK, 16, 1024), dV0 = umma_desc_sw128(sV, 16, 1024);
+            const uint64_t dQ0 = umma_desc_sw128(sQ0, 16, 1024), ddO0 = umma_desc_sw128(sdO0, 16, 1024);
+            const uint64_t dQmn = umma_desc_sw128(sQ0, 16384, 1024), ddOmn = umma_desc_sw128(sdO0, 16384, 1024);
+            auto issue_s = [&](uint32_t gs, bool first, bool last, uint32_t ic) {
+                const uint32_t qs = gs % NQ;
+                mbar_wait(smem_u32(&bars.qf[qs]), (gs / NQ) & 1);
+                if (first) mbar_wait(smem_u32(&bars.kf), ic & 1);
+                tc_fence_after();
+                if (leader) {
+                    const uint64_t b0 = dQ0 + static_cast<uint64_t>((qs * C::kT) >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                        mma_ss(tmem + C::tR + 128 * (gs & 1), dK0 + o, b0 + o, idS, kk > 0);
+                    }
+                    mma_commit(smem_u32(&bars.sf));
+                    if (last) mma_commit(smem_u32(&bars.kfree));
+                }
+                __syncwarp();
+            };
+            auto issue_dp = [&](uint32_t gs, bool first, bool last, uint32_t ic) {
+                const uint32_t os = gs % NO;
+                mbar_wait(smem_u32(&bars.of[os]), (gs / NO) & 1);
+                if (first) mbar_wait(smem_u32(&bars.vf), ic & 1);
+                mbar_wait(smem_u32(&bars.sfr), gs & 1);
+                S2TRACE(13, gs);
+                tc_fence_after();
+                if (leader) {
+                    const uint64_t b0 = ddO0 + static_cast<uint64_t>((os * C::kT) >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                        mma_ss(tmem + C::tR + 128 * (gs & 1), dV0 + o, b0 + o, idS, kk > 0);
+                    }
+                    mma_commit(smem_u32(&bars.dpf));
+                    if (last) mma_commit(smem_u32(&bars.vfree));
+                }
+                __syncwarp();
+            };
+            auto issue_acc = [&](uint32_t gs, bool first, bool last, uint32_t ic) {
+                mbar_wait(smem_u32(&bars.pds), gs & 1);  // P^T(gs), dS^T(gs) in TMEM
+                if (first && ic > 0) mbar_wait(smem_u32(&bars.acce), (ic - 1) & 1);
+                S2TRACE(2, gs);
+                tc_fence_after();
+                const uint32_t reg = C::tR + 128 * (gs & 1);
+                const uint32_t os = gs % NO, qs = gs % NQ;
+                if (leader) {
+                    const uint64_t bo = ddOmn + static_cast<uint64_t>((os * C::kT) >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)  // K-dim: the step's 128 q rows; P^T at +16
+                        mma_ts(tmem + C::tdV, tmem + reg + (kk >> 1) * 32 + 16 + (kk & 1) * 8,
+                               bo + ((kk * 2048) >> 4), idA, (!first || kk > 0) ? 1u : 0u);
+                    mma_commit(smem_u32(&bars.oe[os]));  // dO(gs) read (dP^T(gs), dV(gs))
+                    const uint64_t bq = dQmn + static_cast<uint64_t>((qs * C::kT) >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)  // dS^T at +0
+                        mma_ts(tmem + C::tdK, tmem + reg + (kk >> 1) * 32 + (kk & 1) * 8,
+                               bq + ((kk * 2048) >> 4), idA, (!first || kk > 0) ? 1u : 0u);
+                    mma_commit(smem_u32(&bars.qe[qs]));  // Q(gs) read (S^T(gs), dK(gs))
+                    if (last) mma_commit(smem_u32(&bars.accf));
+                }
+                __syncwarp();
+                S2TRACE(3, gs);
+            };
+            // the previous step's (first, last, item index) for its dV / dK
+            bool p_first = false, p_last = false, have_prev = false;
+            uint32_t p_ic = 0, g = 0, ic = 0;
+            int i = i_beg;
+            while (i < i_end && warp_uniform(items[i].nsteps128) == 0) ++i;
+            if (i < i_end) {
+                int ns = warp_uniform(items[i].nsteps128);
+                issue_s(0, true, ns == 1, 0);
+                while (true) {
+                    for (int n = 0; n < ns; ++n, ++g) {
+                        S2TRACE(0, g);
+                        // dP^T(g) (on the elementwise warps' critical path) first unless the
+                        // previous step's dV / dK are ready while S^T(g) is still unread
+                        if (S2_DKV2_DYN && have_prev) {
+                            bool dp_done = false;
+                            while (true) {
+                                if (mbar_test(smem_u32(&bars.sfr), g & 1)) {
+                                    issue_dp(g, n == 0, n == ns - 1, ic);
+                                    dp_done = true;
+                                    break;
+                                }
+                                if (mbar_test(smem_u32(&bars.pds), (g - 1) & 1)) break;
+                            }
+                            issue_acc(g - 1, p_first, p_last, p_ic);
+                            if (!dp_done) issue_dp(g, n == 0, n == ns - 1, ic);
+                        } else {
+                            issue_dp(g, n == 0, n == ns - 1, ic);
+                            if (have_prev) issue_acc(g - 1, p_first, p_last, p_ic);
+                        }
+                        // the next step: n+1 of this item, or the first of the next item
+                        int ni = i, nn = n + 1, nns = ns;
+                        uint32_t nic = ic;
+                        if (nn == ns) {
+                            ni = i + 1;
+                            while (ni < i_end && warp_uniform(items[ni].nsteps128) == 0) ++ni;
+                            nn = 0;
+                            nic = ic + 1;
+                            nns = ni < i_end ? warp_uniform(items[ni].nsteps128) : 0;
+                        }
+                        if (ni < i_end) issue_s(g + 1, nn == 0, nn == nns - 1, nic);
+                        S2TRACE(1, g);
+                        have_prev = true;
+                        p_first = n == 0;
+                        p_last = n == ns - 1;
+                        p_ic = ic;
+                    }
+                    ++ic;
+                    ++i;
+                    while (i < i_end && warp_uniform(items[i].nsteps128) == 0) ++i;
+                    if (i >= i_end) break;
+                    ns = warp_uniform(items[i].nsteps128);
+                }
+                issue_acc(g - 1, p_first, p_last, p_ic);
+            }
+        } else if (warp == 1) {  // single issuer (S2_DKV2_SPLIT=0)
             // -------------------------------------------------------- MMA issuer
             constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
             constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
@@ -1541,7 +1778,7 @@ __global__ void __launch_bounds__(768, 1)
         const float sl2 = p.scale_log2;
         const uint64_t sl2v = f2_pack(sl2, sl2);
         const int cg = (kr & 63) >> 4;
-        uint32_t g = 0;
+        uint32_t g = 0, g_done = 0;
         for (int i = i_beg; i < i_end; ++i) {
             const BwdItem it = items[i];
             if (it.nsteps128 == 0) continue;
@@ -1568,6 +1805,16 @@ __global__ void __launch_bounds__(768, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bars.sfr));  // dP^T(n) may now be computed over S^T(n)
+                // The two halves of the elementwise warps (X: q columns [64X, 64X+64))
+                // take turns on the exponentials -- X0(n), X1(n), X0(n+1), ... -- so each
+                // runs with the MUFU pipe to itself while the other does its dS / P
+                // packing (all 16 warps exponentiating together was MUFU-bound for
+                // ~1.3K cycles, then issue-bound for ~0.9K, per step)
+                const int X = w >> 1;
+                if (S2_DKV2_ALT) {
+                    if (X == 1) named_bar_sync(2, 512);
+                    else if (g_done > 0) named_bar_sync(3, 512);
+                }
                 if (tid == 256) S2TRACE(9, g);
                 const int dbg = p.debug;  // timing ablations (wrong results when != 0)
                 if (dbg & 64) {
@@ -1603,6 +1850,8 @@ __global__ void __launch_bounds__(768, 1)
                         }
                     }
                 }
+                if (S2_DKV2_ALT) named_bar_arrive(2 + X, 512);
+                ++g_done;
                 if (tid == 256) S2TRACE(10, g);
                 mbar_wait(smem_u32(&bars.dpf), g & 1);
                 if (tid == 256) S2TRACE(11, g);
@@ -1634,6 +1883,7 @@ __global__ void __launch_bounds__(768, 1)
                 if (tid == 256) S2TRACE(7, g);
             }
         }
+        if (S2_DKV2_ALT && (w >> 1) == 0 && g_done > 0) named_bar_sync(3, 512);  // X1's last arrival
     }
     tc_fence_before();
     __syncthreads();
