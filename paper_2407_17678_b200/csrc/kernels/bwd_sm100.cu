@@ -144,6 +144,11 @@ struct BwdCfg {
 #ifndef S2_DQ_NST
 #define S2_DQ_NST 4
 #endif
+// dQ kernel: a dedicated epilogue warpgroup (warps 12-15) drains and stores the
+// accumulator while the elementwise warps start the next item
+#ifndef S2_DQ_EPI_WG
+#define S2_DQ_EPI_WG 0
+#endif
     static constexpr int kNSTq = S2_DQ_NST;
     static constexpr int kDqStage = 2 * kTile64;
     static constexpr int kDqBars = 256 + 1024;  // barriers | fused prep: 2 x 128 partial row dots
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 template <int D>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(S2_DQ_EPI_WG ? 512 : 384, 1)
     s2_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                      const __grid_constant__ CUtensorMap tmdQ, const __grid_constant__ CUtensorMap /*unused*/,
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(384, 1)
         mbar_init(smem_u32(&bar_qf), 1);
         mbar_init(smem_u32(&bar_qe), 1);
         mbar_init(smem_u32(&bar_af), 1);
-        mbar_init(smem_u32(&bar_ae), 256);
+        mbar_init(smem_u32(&bar_ae), S2_DQ_EPI_WG ? 128 : 256);
         for (int i = 0; i < NST; ++i) {
             mbar_init(smem_u32(&bar_sf[i]), 1);
             mbar_init(smem_u32(&bar_se[i]), 1);
@@ -734,8 +739,53 @@ __global__ void __launch_bounds__(384, 1)
                 __syncwarp();
             }
         }
+    } else if (S2_DQ_EPI_WG && warp >= 12) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 152;" ::: "memory");
+        // ------------------------------------------------------------ epilogue
+        // dQ accumulator -> registers in two 64-column halves (released after the
+        // second), x scale, bf16 into the swizzled staging tile, TMA store; the
+        // elementwise warps meanwhile start the next item
+        const int r = tid & 127;
+        const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        uint32_t it_cnt = 0;
+        for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
+            const FwdItem it = items[i];
+            mbar_wait(smem_u32(&bar_af), it_cnt & 1);
+            tc_fence_after();
+            if (tid == 384) bulk_wait_read0();  // the previous item's store has read the staging tile
+            named_bar_sync(2, 128);
+            const float sc = it.chunk_cnt > 0 ? p.scale : 0.f;  // no chunks: dQ = 0
+#pragma unroll
+            for (int h = 0; h < D / 64; ++h) {
+                uint32_t acc[64];
+                tmem_ld32(tmem + 384 + h * 64 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(acc));
+                tmem_ld32(tmem + 384 + h * 64 + 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(acc + 32));
+                tmem_ld_wait();
+                if (h == D / 64 - 1) {
+                    tc_fence_before();
+                    mbar_arrive(smem_u32(&bar_ae));  // the next item's first dQ MMA may overwrite it
+                }
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of this 64-column slice
+                    const uint32_t w0 = pack_bf16(__uint_as_float(acc[8 * c]) * sc, __uint_as_float(acc[8 * c + 1]) * sc);
+                    const uint32_t w1 = pack_bf16(__uint_as_float(acc[8 * c + 2]) * sc, __uint_as_float(acc[8 * c + 3]) * sc);
+                    const uint32_t w2 = pack_bf16(__uint_as_float(acc[8 * c + 4]) * sc, __uint_as_float(acc[8 * c + 5]) * sc);
+                    const uint32_t w3 = pack_bf16(__uint_as_float(acc[8 * c + 6]) * sc, __uint_as_float(acc[8 * c + 7]) * sc);
+                    sts_u4(sOut + h * 16384 + r * 128 + ((c ^ (r & 7)) << 4), w0, w1, w2, w3);
+                }
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(2, 128);
+            if (tid == 384) {
+#pragma unroll
+                for (int sb = 0; sb < C::kSub; ++sb)
+                    tma_store_3d(&tmdQ, sOut + sb * 16384, sb * 64, it.qtile * 128, it.bh);
+                bulk_commit();
+            }
+        }
+        if (tid == 384) bulk_wait0();  // the staging tile must outlive the store
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(S2_DQ_EPI_WG ? 152 : 224) : "memory");
         const int wg = (warp >> 2) - 1;  // key-column half of each 64-key chunk
         const int r = tid & 127;          // query row == TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -828,41 +878,43 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_arrive(smem_u32(&bar_p[b]));
                 if (tid == 128) S2TRACE(7, n_glob);
             }
-            mbar_wait(smem_u32(&bar_af), it_cnt & 1);
-            tc_fence_after();
-            // TMEM -> registers (accumulator released), bf16 into the swizzled
-            // staging tile, TMA store of the 128 x D tile (rows past seq_len clipped)
-            uint32_t acc[D / 2];
+            if (!S2_DQ_EPI_WG) {
+                mbar_wait(smem_u32(&bar_af), it_cnt & 1);
+                tc_fence_after();
+                // TMEM -> registers (accumulator released), bf16 into the swizzled
+                // staging tile, TMA store of the 128 x D tile (rows past seq_len clipped)
+                uint32_t acc[D / 2];
 #pragma unroll
-            for (int c = 0; c < D / 64; ++c)
-                tmem_ld32(tmem + 384 + wg * (D / 2) + c * 32 + lane_off,
-                          *reinterpret_cast<uint32_t(*)[32]>(acc + 32 * c));
-            tmem_ld_wait();
-            tc_fence_before();
-            mbar_arrive(smem_u32(&bar_ae));
-            // the previous item's store has read the staging tile (long ago)
-            if (tid == 128) bulk_wait_read0();
-            named_bar_sync(1, 256);
-            const float sc = it.chunk_cnt > 0 ? p.scale : 0.f;  // no chunks: dQ = 0
+                for (int c = 0; c < D / 64; ++c)
+                    tmem_ld32(tmem + 384 + wg * (D / 2) + c * 32 + lane_off,
+                              *reinterpret_cast<uint32_t(*)[32]>(acc + 32 * c));
+                tmem_ld_wait();
+                tc_fence_before();
+                mbar_arrive(smem_u32(&bar_ae));
+                // the previous item's store has read the staging tile (long ago)
+                if (tid == 128) bulk_wait_read0();
+                named_bar_sync(1, 256);
+                const float sc = it.chunk_cnt > 0 ? p.scale : 0.f;  // no chunks: dQ = 0
 #pragma unroll
-            for (int c = 0; c < D / 16; ++c) {  // my 16-byte chunks: global chunk index g
-                const int g = wg * (D / 16) + c;
-                const uint32_t w0 = pack_bf16(__uint_as_float(acc[8 * c]) * sc, __uint_as_float(acc[8 * c + 1]) * sc);
-                const uint32_t w1 = pack_bf16(__uint_as_float(acc[8 * c + 2]) * sc, __uint_as_float(acc[8 * c + 3]) * sc);
-                const uint32_t w2 = pack_bf16(__uint_as_float(acc[8 * c + 4]) * sc, __uint_as_float(acc[8 * c + 5]) * sc);
-                const uint32_t w3 = pack_bf16(__uint_as_float(acc[8 * c + 6]) * sc, __uint_as_float(acc[8 * c + 7]) * sc);
-                sts_u4(sOut + (g >> 3) * 16384 + r * 128 + (((g & 7) ^ (r & 7)) << 4), w0, w1, w2, w3);
-            }
-            fence_proxy_async_smem();
-            named_bar_sync(1, 256);
-            if (tid == 128) {
+                for (int c = 0; c < D / 16; ++c) {  // my 16-byte chunks: global chunk index g
+                    const int g = wg * (D / 16) + c;
+                    const uint32_t w0 = pack_bf16(__uint_as_float(acc[8 * c]) * sc, __uint_as_float(acc[8 * c + 1]) * sc);
+                    const uint32_t w1 = pack_bf16(__uint_as_float(acc[8 * c + 2]) * sc, __uint_as_float(acc[8 * c + 3]) * sc);
+                    const uint32_t w2 = pack_bf16(__uint_as_float(acc[8 * c + 4]) * sc, __uint_as_float(acc[8 * c + 5]) * sc);
+                    const uint32_t w3 = pack_bf16(__uint_as_float(acc[8 * c + 6]) * sc, __uint_as_float(acc[8 * c + 7]) * sc);
+                    sts_u4(sOut + (g >> 3) * 16384 + r * 128 + (((g & 7) ^ (r & 7)) << 4), w0, w1, w2, w3);
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(1, 256);
+                if (tid == 128) {
 #pragma unroll
-                for (int sb = 0; sb < C::kSub; ++sb)
-                    tma_store_3d(&tmdQ, sOut + sb * 16384, sb * 64, it.qtile * 128, it.bh);
-                bulk_commit();
+                    for (int sb = 0; sb < C::kSub; ++sb)
+                        tma_store_3d(&tmdQ, sOut + sb * 16384, sb * 64, it.qtile * 128, it.bh);
+                    bulk_commit();
+                }
             }
         }
-        if (tid == 128) bulk_wait0();  // the staging tile must outlive the store
+        if (!S2_DQ_EPI_WG && tid == 128) bulk_wait0();  // the staging tile must outlive the store
     }
     tc_fence_before();
     __syncthreads();
@@ -1973,9 +2025,11 @@ cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CU
     }
     if (D == 128)
         return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<128>, BwdCfg<128>::kDkvSmem, grid, q, dout, k, v, o0, o1, pp, stream)
-                          : launch_bwd(s2_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmem, grid, q, dout, k, v, o0, o1, pp, stream);
+                          : launch_bwd(s2_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmem, grid, q, dout, k, v, o0, o1, pp, stream,
+                                       S2_DQ_EPI_WG ? 512 : 384);
     if (D == 64)
         return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<64>, BwdCfg<64>::kDkvSmem, grid, q, dout, k, v, o0, o1, pp, stream)
-                          : launch_bwd(s2_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmem, grid, q, dout, k, v, o0, o1, pp, stream);
+                          : launch_bwd(s2_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmem, grid, q, dout, k, v, o0, o1, pp, stream,
+                                       S2_DQ_EPI_WG ? 512 : 384);
     return cudaErrorInvalidValue;
 }
