@@ -14,7 +14,8 @@ cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CU
                                 const void* entries, const float* lse2, const float* delta,
                                 int N, int Npad, int hpg, float scale, cudaStream_t stream,
                                 void* g0, void* g1, const void* fused_o = nullptr,
-                                const void* fused_dout = nullptr, const float* fused_lse = nullptr);
+                                const void* fused_dout = nullptr, const float* fused_lse = nullptr,
+                                float* fused_delta = nullptr, float* fused_lse2 = nullptr);
 
 using namespace s2;
 
@@ -118,7 +119,7 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
             return s2_launch_bwd_sm100(dq_v1 ? 1 : 2, D, q128, do128, dq_v1 ? mk4 : mk, dq_v1 ? mv4 : mv, mdq, mdq,
                                        w->fwd.ptr, w->fwd_sched.as<int>(), w->grid, L->d_chunks.ptr, lse2, delta, N,
                                        Npad, hpg, float(scale), st, nullptr, nullptr, fused ? f.out : nullptr,
-                                       a->dout, f.lse);
+                                       a->dout, f.lse, delta, lse2);
         };
         auto run_dkv = [&]() {
             ProfScope prof("bwd_dkv_sm100", st);

@@ -110,6 +110,8 @@ struct BwdParams {
     const __nv_bfloat16* o;    // nullptr: not fused (the prep kernel ran)
     const __nv_bfloat16* dout;
     const float* lse;          // the forward's lse (natural log) [num_qbh][N]
+    float* delta_w;            // = delta / lse2 above, writable (fused prep only)
+    float* lse2_w;
 };
 
 #define S2TRACE(slot, n)                                                       \
@@ -144,11 +146,7 @@ struct BwdCfg {
 #ifndef S2_DQ_NST
 #define S2_DQ_NST 4
 #endif
-// dQ kernel: a dedicated epilogue warpgroup (warps 12-15) drains and stores the
-// accumulator while the elementwise warps start the next item
-#ifndef S2_DQ_EPI_WG
-#define S2_DQ_EPI_WG 0
-#endif
+
     static constexpr int kNSTq = S2_DQ_NST;
     static constexpr int kDqStage = 2 * kTile64;
     static constexpr int kDqBars = 256 + 1024;  // barriers | fused prep: 2 x 128 partial row dots
@@ -570,7 +568,7 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 template <int D>
-__global__ void __launch_bounds__(S2_DQ_EPI_WG ? 512 : 384, 1)
+__global__ void __launch_bounds__(384, 1)
     s2_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                      const __grid_constant__ CUtensorMap tmdQ, const __grid_constant__ CUtensorMap /*unused*/,
@@ -607,7 +605,7 @@ __global__ void __launch_bounds__(S2_DQ_EPI_WG ? 512 : 384, 1)
         mbar_init(smem_u32(&bar_qf), 1);
         mbar_init(smem_u32(&bar_qe), 1);
         mbar_init(smem_u32(&bar_af), 1);
-        mbar_init(smem_u32(&bar_ae), S2_DQ_EPI_WG ? 128 : 256);
+        mbar_init(smem_u32(&bar_ae), 256);
         for (int i = 0; i < NST; ++i) {
             mbar_init(smem_u32(&bar_sf[i]), 1);
             mbar_init(smem_u32(&bar_se[i]), 1);
@@ -739,53 +737,8 @@ __global__ void __launch_bounds__(S2_DQ_EPI_WG ? 512 : 384, 1)
                 __syncwarp();
             }
         }
-    } else if (S2_DQ_EPI_WG && warp >= 12) {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 152;" ::: "memory");
-        // ------------------------------------------------------------ epilogue
-        // dQ accumulator -> registers in two 64-column halves (released after the
-        // second), x scale, bf16 into the swizzled staging tile, TMA store; the
-        // elementwise warps meanwhile start the next item
-        const int r = tid & 127;
-        const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-        uint32_t it_cnt = 0;
-        for (int i = p.sched[blockIdx.x]; i < p.sched[blockIdx.x + 1]; ++i, ++it_cnt) {
-            const FwdItem it = items[i];
-            mbar_wait(smem_u32(&bar_af), it_cnt & 1);
-            tc_fence_after();
-            if (tid == 384) bulk_wait_read0();  // the previous item's store has read the staging tile
-            named_bar_sync(2, 128);
-            const float sc = it.chunk_cnt > 0 ? p.scale : 0.f;  // no chunks: dQ = 0
-#pragma unroll
-            for (int h = 0; h < D / 64; ++h) {
-                uint32_t acc[64];
-                tmem_ld32(tmem + 384 + h * 64 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(acc));
-                tmem_ld32(tmem + 384 + h * 64 + 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(acc + 32));
-                tmem_ld_wait();
-                if (h == D / 64 - 1) {
-                    tc_fence_before();
-                    mbar_arrive(smem_u32(&bar_ae));  // the next item's first dQ MMA may overwrite it
-                }
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of this 64-column slice
-                    const uint32_t w0 = pack_bf16(__uint_as_float(acc[8 * c]) * sc, __uint_as_float(acc[8 * c + 1]) * sc);
-                    const uint32_t w1 = pack_bf16(__uint_as_float(acc[8 * c + 2]) * sc, __uint_as_float(acc[8 * c + 3]) * sc);
-                    const uint32_t w2 = pack_bf16(__uint_as_float(acc[8 * c + 4]) * sc, __uint_as_float(acc[8 * c + 5]) * sc);
-                    const uint32_t w3 = pack_bf16(__uint_as_float(acc[8 * c + 6]) * sc, __uint_as_float(acc[8 * c + 7]) * sc);
-                    sts_u4(sOut + h * 16384 + r * 128 + ((c ^ (r & 7)) << 4), w0, w1, w2, w3);
-                }
-            }
-            fence_proxy_async_smem();
-            named_bar_sync(2, 128);
-            if (tid == 384) {
-#pragma unroll
-                for (int sb = 0; sb < C::kSub; ++sb)
-                    tma_store_3d(&tmdQ, sOut + sb * 16384, sb * 64, it.qtile * 128, it.bh);
-                bulk_commit();
-            }
-        }
-        if (tid == 384) bulk_wait0();  // the staging tile must outlive the store
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(S2_DQ_EPI_WG ? 152 : 224) : "memory");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
         const int wg = (warp >> 2) - 1;  // key-column half of each 64-key chunk
         const int r = tid & 127;          // query row == TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -827,8 +780,8 @@ __global__ void __launch_bounds__(S2_DQ_EPI_WG ? 512 : 384, 1)
                 dl = live ? dot : 0.f;
                 l2 = live ? l * 1.4426950408889634f : INFINITY;
                 if (wg == 0) {
-                    const_cast<float*>(p.delta)[lrow] = dl;
-                    const_cast<float*>(p.lse2)[lrow] = l2;
+                    p.delta_w[lrow] = dl;
+                    p.lse2_w[lrow] = l2;
                 }
             } else {
                 l2 = p.lse2[lrow];
@@ -878,43 +831,41 @@ __global__ void __launch_bounds__(S2_DQ_EPI_WG ? 512 : 384, 1)
                 mbar_arrive(smem_u32(&bar_p[b]));
                 if (tid == 128) S2TRACE(7, n_glob);
             }
-            if (!S2_DQ_EPI_WG) {
-                mbar_wait(smem_u32(&bar_af), it_cnt & 1);
-                tc_fence_after();
-                // TMEM -> registers (accumulator released), bf16 into the swizzled
-                // staging tile, TMA store of the 128 x D tile (rows past seq_len clipped)
-                uint32_t acc[D / 2];
+            mbar_wait(smem_u32(&bar_af), it_cnt & 1);
+            tc_fence_after();
+            // TMEM -> registers (accumulator released), bf16 into the swizzled
+            // staging tile, TMA store of the 128 x D tile (rows past seq_len clipped)
+            uint32_t acc[D / 2];
 #pragma unroll
-                for (int c = 0; c < D / 64; ++c)
-                    tmem_ld32(tmem + 384 + wg * (D / 2) + c * 32 + lane_off,
-                              *reinterpret_cast<uint32_t(*)[32]>(acc + 32 * c));
-                tmem_ld_wait();
-                tc_fence_before();
-                mbar_arrive(smem_u32(&bar_ae));
-                // the previous item's store has read the staging tile (long ago)
-                if (tid == 128) bulk_wait_read0();
-                named_bar_sync(1, 256);
-                const float sc = it.chunk_cnt > 0 ? p.scale : 0.f;  // no chunks: dQ = 0
+            for (int c = 0; c < D / 64; ++c)
+                tmem_ld32(tmem + 384 + wg * (D / 2) + c * 32 + lane_off,
+                          *reinterpret_cast<uint32_t(*)[32]>(acc + 32 * c));
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(smem_u32(&bar_ae));
+            // the previous item's store has read the staging tile (long ago)
+            if (tid == 128) bulk_wait_read0();
+            named_bar_sync(1, 256);
+            const float sc = it.chunk_cnt > 0 ? p.scale : 0.f;  // no chunks: dQ = 0
 #pragma unroll
-                for (int c = 0; c < D / 16; ++c) {  // my 16-byte chunks: global chunk index g
-                    const int g = wg * (D / 16) + c;
-                    const uint32_t w0 = pack_bf16(__uint_as_float(acc[8 * c]) * sc, __uint_as_float(acc[8 * c + 1]) * sc);
-                    const uint32_t w1 = pack_bf16(__uint_as_float(acc[8 * c + 2]) * sc, __uint_as_float(acc[8 * c + 3]) * sc);
-                    const uint32_t w2 = pack_bf16(__uint_as_float(acc[8 * c + 4]) * sc, __uint_as_float(acc[8 * c + 5]) * sc);
-                    const uint32_t w3 = pack_bf16(__uint_as_float(acc[8 * c + 6]) * sc, __uint_as_float(acc[8 * c + 7]) * sc);
-                    sts_u4(sOut + (g >> 3) * 16384 + r * 128 + (((g & 7) ^ (r & 7)) << 4), w0, w1, w2, w3);
-                }
-                fence_proxy_async_smem();
-                named_bar_sync(1, 256);
-                if (tid == 128) {
+            for (int c = 0; c < D / 16; ++c) {  // my 16-byte chunks: global chunk index g
+                const int g = wg * (D / 16) + c;
+                const uint32_t w0 = pack_bf16(__uint_as_float(acc[8 * c]) * sc, __uint_as_float(acc[8 * c + 1]) * sc);
+                const uint32_t w1 = pack_bf16(__uint_as_float(acc[8 * c + 2]) * sc, __uint_as_float(acc[8 * c + 3]) * sc);
+                const uint32_t w2 = pack_bf16(__uint_as_float(acc[8 * c + 4]) * sc, __uint_as_float(acc[8 * c + 5]) * sc);
+                const uint32_t w3 = pack_bf16(__uint_as_float(acc[8 * c + 6]) * sc, __uint_as_float(acc[8 * c + 7]) * sc);
+                sts_u4(sOut + (g >> 3) * 16384 + r * 128 + (((g & 7) ^ (r & 7)) << 4), w0, w1, w2, w3);
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1, 256);
+            if (tid == 128) {
 #pragma unroll
-                    for (int sb = 0; sb < C::kSub; ++sb)
-                        tma_store_3d(&tmdQ, sOut + sb * 16384, sb * 64, it.qtile * 128, it.bh);
-                    bulk_commit();
-                }
+                for (int sb = 0; sb < C::kSub; ++sb)
+                    tma_store_3d(&tmdQ, sOut + sb * 16384, sb * 64, it.qtile * 128, it.bh);
+                bulk_commit();
             }
         }
-        if (!S2_DQ_EPI_WG && tid == 128) bulk_wait0();  // the staging tile must outlive the store
+        if (tid == 128) bulk_wait0();  // the staging tile must outlive the store
     }
     tc_fence_before();
     __syncthreads();
@@ -1299,14 +1250,11 @@ __global__ void __launch_bounds__(512, 1)
 #ifndef S2_DKV2_ALT
 #define S2_DKV2_ALT 0
 #endif
-// MMA issue: 2 = one issuer, dP^T-first order; 1 = two issuers (S^T / dP^T and
-// dV / dK); 0 = one issuer, S^T-first order
+// MMA issue order: 2 = dP^T-first (default), 0 = S^T-first (the original order).
+// (Two issuers, and a dynamic choice between dP^T and the previous step's dV / dK,
+// measured slower: DESIGN.md section 7.)
 #ifndef S2_DKV2_SPLIT
 #define S2_DKV2_SPLIT 2
-#endif
-// order 2 only: issue the previous step's dV / dK first when they are ready before S^T(g) is read
-#ifndef S2_DKV2_DYN
-#define S2_DKV2_DYN 0
 #endif
 template <int D>
 struct Dkv2Cfg {
@@ -1332,7 +1280,7 @@ __global__ void __launch_bounds__(768, 1)
     if (tid == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1024-B alignment
     struct Bars {
         uint64_t kf, vf, kfree, vfree, qf[NQ], qe[NQ], of[NO], oe[NO], af[NA], ae[NA];
-        uint64_t sf, sfr, dpf, pds, accf, acce, rfree[2];
+        uint64_t sf, sfr, dpf, pds, accf, acce;
         uint4 meta[NA];  // per aux slot: first q row, chunk-0 / chunk-1 masks, query data index
         uint32_t tmem_base;
     };
@@ -1367,8 +1315,6 @@ __global__ void __launch_bounds__(768, 1)
         mbar_init(smem_u32(&bars.pds), 16);
         mbar_init(smem_u32(&bars.accf), 1);
         mbar_init(smem_u32(&bars.acce), 4);
-        mbar_init(smem_u32(&bars.rfree[0]), 1);
-        mbar_init(smem_u32(&bars.rfree[1]), 1);
         fence_mbar_init();
     }
     if (warp == 2) {
@@ -1439,102 +1385,6 @@ __global__ void __launch_bounds__(768, 1)
                         ++g;
                     }
                 }
-            }
-        } else if (warp == 1 && S2_DKV2_SPLIT == 1) {
-            // ---------------------------------------------- MMA issuer A: S^T, dP^T
-            // S^T(g) into region g & 1 once dV(g-2), dK(g-2) have read it (issuer B's
-            // rfree commit), dP^T(g) over it once the elementwise warps have read
-            // S^T(g).  With a second issuer for dV / dK, dP^T(g) is issued as soon as
-            // S^T(g) is read, while the exponentials of step g run (one issuer had
-            // to wait for step g-1's P / dS before it).
-            constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
-            const bool leader = elect_one();
-            const uint64_t dK0 = umma_desc_sw128(sK, 16, 1024), dV0 = umma_desc_sw128(sV, 16, 1024);
-            const uint64_t dQ0 = umma_desc_sw128(sQ0, 16, 1024), ddO0 = umma_desc_sw128(sdO0, 16, 1024);
-            uint32_t g = 0, ic = 0;
-            for (int i = i_beg; i < i_end; ++i) {
-                const int ns = warp_uniform(items[i].nsteps128);
-                if (ns == 0) continue;
-                for (int n = 0; n < ns; ++n) {
-                    const uint32_t gs = g + n;
-                    const uint32_t qs = gs % NQ;
-                    S2TRACE(0, gs);
-                    mbar_wait(smem_u32(&bars.qf[qs]), (gs / NQ) & 1);
-                    if (n == 0) mbar_wait(smem_u32(&bars.kf), ic & 1);
-                    if (gs >= 2) mbar_wait(smem_u32(&bars.rfree[gs & 1]), ((gs >> 1) - 1) & 1);
-                    S2TRACE(4, gs);
-                    tc_fence_after();
-                    if (leader) {
-                        const uint64_t b0 = dQ0 + static_cast<uint64_t>((qs * C::kT) >> 4);
-#pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk) {
-                            const uint32_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-                            mma_ss(tmem + C::tR + 128 * (gs & 1), dK0 + o, b0 + o, idS, kk > 0);
-                        }
-                        mma_commit(smem_u32(&bars.sf));
-                        if (n == ns - 1) mma_commit(smem_u32(&bars.kfree));  // the item's K is read by S^T only
-                    }
-                    __syncwarp();
-                    S2TRACE(1, gs);
-                    // dP^T(gs) over S^T(gs) once the elementwise warps have read it
-                    const uint32_t os = gs % NO;
-                    mbar_wait(smem_u32(&bars.of[os]), (gs / NO) & 1);
-                    if (n == 0) mbar_wait(smem_u32(&bars.vf), ic & 1);
-                    mbar_wait(smem_u32(&bars.sfr), gs & 1);
-                    S2TRACE(13, gs);
-                    tc_fence_after();
-                    if (leader) {
-                        const uint64_t b0 = ddO0 + static_cast<uint64_t>((os * C::kT) >> 4);
-#pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk) {
-                            const uint32_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-                            mma_ss(tmem + C::tR + 128 * (gs & 1), dV0 + o, b0 + o, idS, kk > 0);
-                        }
-                        mma_commit(smem_u32(&bars.dpf));
-                        if (n == ns - 1) mma_commit(smem_u32(&bars.vfree));  // V is read by dP^T only
-                    }
-                    __syncwarp();
-                    S2TRACE(14, gs);
-                }
-                g += ns;
-                ++ic;
-            }
-        } else if (warp == 3 && S2_DKV2_SPLIT == 1) {
-            // ---------------------------------------------- MMA issuer B: dV, dK
-            constexpr uint32_t idA = umma_idesc_bf16(128, D, 0, 1);
-            const bool leader = elect_one();
-            const uint64_t dQmn = umma_desc_sw128(sQ0, 16384, 1024), ddOmn = umma_desc_sw128(sdO0, 16384, 1024);
-            uint32_t g = 0, ic = 0;
-            for (int i = i_beg; i < i_end; ++i) {
-                const int ns = warp_uniform(items[i].nsteps128);
-                if (ns == 0) continue;
-                for (int n = 0; n < ns; ++n, ++g) {
-                    mbar_wait(smem_u32(&bars.pds), g & 1);  // P^T(g), dS^T(g) in TMEM
-                    if (n == 0 && ic > 0) mbar_wait(smem_u32(&bars.acce), (ic - 1) & 1);
-                    S2TRACE(2, g);
-                    tc_fence_after();
-                    const uint32_t reg = C::tR + 128 * (g & 1);
-                    const uint32_t os = g % NO, qs = g % NQ;
-                    if (leader) {
-                        const uint64_t bo = ddOmn + static_cast<uint64_t>((os * C::kT) >> 4);
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk)  // K-dim: the step's 128 q rows; P^T at +16
-                            mma_ts(tmem + C::tdV, tmem + reg + (kk >> 1) * 32 + 16 + (kk & 1) * 8,
-                                   bo + ((kk * 2048) >> 4), idA, (n > 0 || kk > 0) ? 1u : 0u);
-                        mma_commit(smem_u32(&bars.oe[os]));  // dO(g) read (dP^T(g) complete earlier, dV(g))
-                        const uint64_t bq = dQmn + static_cast<uint64_t>((qs * C::kT) >> 4);
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk)  // dS^T at +0
-                            mma_ts(tmem + C::tdK, tmem + reg + (kk >> 1) * 32 + (kk & 1) * 8,
-                                   bq + ((kk * 2048) >> 4), idA, (n > 0 || kk > 0) ? 1u : 0u);
-                        mma_commit(smem_u32(&bars.qe[qs]));        // Q(g) read (S^T(g) complete earlier, dK(g))
-                        mma_commit(smem_u32(&bars.rfree[g & 1]));  // region g & 1 may take S^T(g+2)
-                        if (n == ns - 1) mma_commit(smem_u32(&bars.accf));
-                    }
-                    __syncwarp();
-                    S2TRACE(3, g);
-                }
-                ++ic;
             }
         } else if (warp == 1 && S2_DKV2_SPLIT == 2) {
             // ---------------------------------- MMA issuer, dP^T-first order (default)
@@ -1620,24 +1470,8 @@ __global__ void __launch_bounds__(768, 1)
                 while (true) {
                     for (int n = 0; n < ns; ++n, ++g) {
                         S2TRACE(0, g);
-                        // dP^T(g) (on the elementwise warps' critical path) first unless the
-                        // previous step's dV / dK are ready while S^T(g) is still unread
-                        if (S2_DKV2_DYN && have_prev) {
-                            bool dp_done = false;
-                            while (true) {
-                                if (mbar_test(smem_u32(&bars.sfr), g & 1)) {
-                                    issue_dp(g, n == 0, n == ns - 1, ic);
-                                    dp_done = true;
-                                    break;
-                                }
-                                if (mbar_test(smem_u32(&bars.pds), (g - 1) & 1)) break;
-                            }
-                            issue_acc(g - 1, p_first, p_last, p_ic);
-                            if (!dp_done) issue_dp(g, n == 0, n == ns - 1, ic);
-                        } else {
-                            issue_dp(g, n == 0, n == ns - 1, ic);
-                            if (have_prev) issue_acc(g - 1, p_first, p_last, p_ic);
-                        }
+                        issue_dp(g, n == 0, n == ns - 1, ic);
+                        if (have_prev) issue_acc(g - 1, p_first, p_last, p_ic);
                         // the next step: n+1 of this item, or the first of the next item
                         int ni = i, nn = n + 1, nns = ns;
                         uint32_t nic = ic;
@@ -1995,7 +1829,7 @@ cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CU
                                 const void* entries, const float* lse2, const float* delta,
                                 int N, int Npad, int hpg, float scale, cudaStream_t stream,
                                 void* g0, void* g1, const void* fused_o, const void* fused_dout,
-                                const float* fused_lse) {
+                                const float* fused_lse, float* fused_delta, float* fused_lse2) {
     if (grid == 0) return cudaSuccess;
     const float sl2 = scale * 1.4426950408889634f;
     // debug bit 8 selects which kernel records the trace (0: dK/dV, 8: dQ)
@@ -2003,7 +1837,7 @@ cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CU
     BwdParams pp{items, sched, entries, lse2, delta, static_cast<__nv_bfloat16*>(g0), static_cast<__nv_bfloat16*>(g1),
                  N, Npad, hpg, sl2, scale, tr, g_debug & ~8,
                  which == 1 ? static_cast<const __nv_bfloat16*>(fused_o) : nullptr,
-                 static_cast<const __nv_bfloat16*>(fused_dout), fused_lse};
+                 static_cast<const __nv_bfloat16*>(fused_dout), fused_lse, fused_delta, fused_lse2};
     if (g_debug & 4) grid = 1;  // debug: isolate one CTA from memory-system contention
     if (which == 3) {  // dK/dV over 128-row q steps (q/do: 4-D 128-row maps; g0 = dK, g1 = dV)
         if (D == 128)
@@ -2025,11 +1859,9 @@ cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CU
     }
     if (D == 128)
         return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<128>, BwdCfg<128>::kDkvSmem, grid, q, dout, k, v, o0, o1, pp, stream)
-                          : launch_bwd(s2_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmem, grid, q, dout, k, v, o0, o1, pp, stream,
-                                       S2_DQ_EPI_WG ? 512 : 384);
+                          : launch_bwd(s2_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmem, grid, q, dout, k, v, o0, o1, pp, stream);
     if (D == 64)
         return which == 0 ? launch_bwd(s2_bwd_dkv_kernel<64>, BwdCfg<64>::kDkvSmem, grid, q, dout, k, v, o0, o1, pp, stream)
-                          : launch_bwd(s2_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmem, grid, q, dout, k, v, o0, o1, pp, stream,
-                                       S2_DQ_EPI_WG ? 512 : 384);
+                          : launch_bwd(s2_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmem, grid, q, dout, k, v, o0, o1, pp, stream);
     return cudaErrorInvalidValue;
 }
