@@ -276,6 +276,36 @@ def test_f32_tiled_kernel_blocks_and_tails(N, S, d, rowwise, monkeypatch):
     np.testing.assert_allclose(t.lse, rl, **F32_TOL)
 
 
+@pytest.mark.parametrize("D,S,kv", [(64, 64, 2), (40, 32, 1), (128, 128, 4)])
+def test_f32_tiled_kernel_gqa_batch_units(D, S, kv):
+    """fp32 forward with GQA (query heads per kv head 2 / 4), batch 2 and a unit
+    subset: every (batch, kv group) of the tiled kernel against the oracle at 1e-4,
+    and the unit-subset call bit-identical to the full call."""
+    torch = _torch()
+    H, N, B = 4, 777, 2
+    cfg = single(N, S, H, 2, 3, kv=kv)
+    rng = np.random.default_rng(D + S)
+    q = rng.uniform(-1, 1, B * H * N * D).astype(np.float32)
+    k, v = (rng.uniform(-1, 1, B * kv * N * D).astype(np.float32) for _ in range(2))
+    T = lambda x, h: torch.from_numpy(x).reshape(B, h, N, D).cuda()  # noqa: E731
+    plan = s2.Plan.from_config(cfg)
+    out, lse = s2.s2_attn_fwd(plan, T(q, H), T(k, kv), T(v, kv))
+    torch.cuda.synchronize()
+    rp, ci = oracle.csr_all(cfg)
+    ro, rl = oracle.attn_fwd(q, k, v, rp, ci, B, H, kv, N, D, S)
+    np.testing.assert_allclose(out.cpu().numpy().ravel(), ro, **F32_TOL)
+    np.testing.assert_allclose(lse.cpu().numpy().ravel(), rl, **F32_TOL)
+    hpg = H // kv
+    units = np.array([2 * kv - 1, 0], np.int32)  # (b=1, g=kv-1), (b=0, g=0)
+    idx = torch.as_tensor(units, dtype=torch.long)
+    qu = T(q, H).reshape(B * kv, hpg, N, D)[idx].contiguous()
+    ku = T(k, kv).reshape(B * kv, N, D)[idx].contiguous()
+    vu = T(v, kv).reshape(B * kv, N, D)[idx].contiguous()
+    ou, _ = s2.s2_attn_fwd(plan, qu, ku, vu, unit_ids=units)
+    torch.cuda.synchronize()
+    assert torch.equal(ou.cpu(), out.reshape(B * kv, hpg, N, D).cpu()[idx])
+
+
 @pytest.mark.parametrize("d", [32, 96, 256])
 def test_bf16_other_head_dims_take_the_simt_kernel_and_match_oracle(d):
     """bf16 with a head dim the tensor-core kernel does not take (not 64 / 128) runs
