@@ -198,9 +198,15 @@ static bool pair2_enabled() {
     return e && e[0] == '1';
 }
 
-static int dkv_group() {
+// dK/dV schedule: units (kv heads) are swept in groups, LPT inside a group, so the
+// Q / dO rows the CTAs stream concurrently belong to fewer heads and stay in L2.
+// Default: two halves once there are 16+ units (cfg3: dK/dV 1.26 -> 1.23 ms; four or
+// more groups lose to the LPT imbalance at group boundaries).  S2_DKV_GROUP=<units
+// per group> overrides, 0 = one group.
+static int dkv_group(int num_units) {
     const char* e = getenv("S2_DKV_GROUP");
-    return e ? atoi(e) : 0;
+    if (e) return atoi(e);
+    return num_units >= 16 ? (num_units + 1) / 2 : 0;
 }
 
 // per-item overhead of the LPT cost model, in step units (tuning knob: env
@@ -342,7 +348,7 @@ WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* 
         auto bwd_cost = [](const s2dev::BwdItem& a) { return int64_t(a.nsteps); };
         const std::vector<int32_t> off_bwd = schedule_items(
             bi, grid, bwd_cost, [](const s2dev::BwdItem& a) { return a.kvbh; }, sched_overhead("S2_SCHED_OVH_DKV", 4),
-            dkv_group());
+            dkv_group(static_cast<int>(units.size())));
         w->num_fwd = static_cast<int>(fi.size());
         w->num_bwd = static_cast<int>(bi.size());
         w->grid = grid;
