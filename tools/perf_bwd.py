@@ -59,4 +59,4 @@ nk = ctypes.c_int()
 L.s2_profile_collect(16, names, tot, cnt, ctypes.byref(nk))
 L.s2_profile_enable(0)
 print("  kernels: " + ", ".join(
-    f"{names.raw[32*i:32*i+32].split(b'\\0')[0].decode()} {tot[i]/cnt[i]:.3f} ms" for i in range(nk.value)))
+    f"{names.raw[32*i:32*i+32].split(bytes(1))[0].decode()} {tot[i]/cnt[i]:.3f} ms" for i in range(nk.value)))
