@@ -63,3 +63,13 @@ if (t[12] > 0).sum() > 10:  # built with -DS2_FWD_DETAIL_TRACE
 if (t[16] > 0).sum() > 40:
     print(f"softmax0 gap split: P arrive -> next chunk's loop top {m(t[16, lo + 1:hi + 1] - t[8, lo:hi]):.0f}, "
           f"loop top -> wait {m(t[4, lo + 1:hi + 1] - t[16, lo + 1:hi + 1]):.0f}")
+
+# period distribution of the S issuer's chunk starts (all traced chunks)
+nk = int((t[0] > 0).sum())
+if nk > 40:
+    per = np.diff(t[0, :nk]).astype(np.float64)
+    q = np.percentile(per, [10, 50, 75, 90, 99])
+    print(f"chunk period: mean {per.mean():.0f}, p10/50/75/90/99 {q.round(0).tolist()}; "
+          f"share of time in chunks > 1.5x median {per[per > 1.5 * np.median(per)].sum() / per.sum():.1%}")
+    big = per > 1.5 * np.median(per)
+    print(f"  chunks > 1.5x median: {big.sum()} of {len(per)}; their mean {per[big].mean():.0f}")
