@@ -73,3 +73,12 @@ if nk > 40:
           f"share of time in chunks > 1.5x median {per[per > 1.5 * np.median(per)].sum() / per.sum():.1%}")
     big = per > 1.5 * np.median(per)
     print(f"  chunks > 1.5x median: {big.sum()} of {len(per)}; their mean {per[big].mean():.0f}")
+    # where the slow chunks spend their time (S issuer view): chunk k's period is
+    # t0[k+1] - t0[k] = wait K(k) + issue S(k) (incl. the S-half waits) + gap to chunk k+1
+    idx = np.where(big)[0]
+    wk = (t[1] - t[0]).astype(np.float64)
+    iss = (t[2] - t[1]).astype(np.float64)
+    gap = (np.roll(t[0], -1) - t[2]).astype(np.float64)
+    print(f"  slow chunks: wait K {np.median(wk[idx]):.0f}, S issue incl. half waits {np.median(iss[idx]):.0f}, "
+          f"gap to next {np.median(gap[idx]):.0f}  (all chunks: {np.median(wk[:nk]):.0f} / {np.median(iss[:nk]):.0f} / "
+          f"{np.median(gap[:nk - 1]):.0f})")
