@@ -168,10 +168,11 @@ int s2_plan_head_nnz(const s2_plan* plan, int head, int64_t* nnz);
  * (test_attention.cpp:124-132).
  *
  * Kernels: bf16 with head_dim 64 / 128 and block_size % 16 == 0 runs the
- * tcgen05 kernel (the only shapes s2_attn_bwd supports); every other bf16 /
- * fp32 case runs an fp32-FFMA kernel -- shared-memory tiles for
- * head_dim <= 256, one warp per row up to 2048 -- with no tensor cores and no
- * backward (S2_ERR_UNSUPPORTED); head_dim > 2048 fails with S2_ERR_UNSUPPORTED.
+ * tcgen05 kernel; every other bf16 / fp32 case runs an fp32-FFMA kernel --
+ * shared-memory tiles for head_dim <= 256, one warp per row up to 2048 -- with
+ * no tensor cores; head_dim > 2048 fails with S2_ERR_UNSUPPORTED.  s2_attn_bwd
+ * follows the same split, its fp32-FFMA kernels taking head_dim <= 128
+ * (S2_ERR_UNSUPPORTED above).
  *
  * Units: the head-parallel partitioner works on (batch, kv-group) units,
  * u = b*num_kv_heads + g.  unit_ids == NULL processes every unit and the
@@ -217,7 +218,11 @@ int s2_attn_fwd_peers(s2_plan* plan, const s2_attn_args* args, int num_peers, vo
 
 /* ---- backward (no reference symbol: SPEC.md:262) ------------------------ */
 /* dQ kernel walks the CSR tile list, dK/dV kernel walks the transposed (CSC)
- * tile list; every dK/dV tile is owned by exactly one CTA (no atomics). */
+ * tile list; every dK/dV tile is owned by exactly one CTA (no atomics).
+ * bf16, head_dim 64 / 128, block_size % 16 == 0: tcgen05 kernels (bwd_sm100.cu);
+ * other bf16 / fp32 shapes with head_dim <= 128: fp32-FFMA tile kernels over
+ * the plan's CSR / CSC (bwd_simt.cu); head_dim > 128 otherwise:
+ * S2_ERR_UNSUPPORTED. */
 typedef struct s2_attn_bwd_args {
     s2_attn_args fwd; /* q, k, v, out (forward output), lse as written by fwd */
     const void* dout;

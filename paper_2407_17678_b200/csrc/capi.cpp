@@ -96,6 +96,36 @@ int ensure_csr_uploaded(s2_plan* p) {
     return S2_OK;
 }
 
+// the transposed lists of every head (ascending query blocks per key block), as
+// s2_layout_build_csc / the reference's to_csr of the transposed mask
+int ensure_csc_uploaded(s2_plan* p) {
+    if (int rc = check_device(p)) return rc;
+    if (p->device < 0) cudaGetDevice(&p->device);
+    if (p->csc_uploaded) return S2_OK;
+    const int H = p->num_heads, B = p->num_blocks;
+    std::vector<int> cp(static_cast<size_t>(H) * (B + 1), 0);
+    std::vector<int> ri;
+    std::vector<int64_t> off(H);
+    for (int h = 0; h < H; ++h) {
+        const Csr& c = p->csr[h];
+        int* col = cp.data() + static_cast<size_t>(h) * (B + 1);
+        for (int x : c.idx) ++col[x + 1];
+        for (int b = 0; b < B; ++b) col[b + 1] += col[b];
+        off[h] = static_cast<int64_t>(ri.size());
+        ri.resize(ri.size() + c.idx.size());
+        std::vector<int> fill(col, col + B);
+        for (int r = 0; r < B; ++r)  // rows ascending -> each column's rows ascending
+            for (int e = c.ptr[r]; e < c.ptr[r + 1]; ++e) ri[off[h] + fill[c.idx[e]]++] = r;
+    }
+    cudaError_t e;
+    if ((e = upload(p->d_col_ptr, cp.data(), cp.size() * sizeof(int))) != cudaSuccess ||
+        (e = upload(p->d_row_idx, ri.data(), ri.size() * sizeof(int))) != cudaSuccess ||
+        (e = upload(p->d_row_off, off.data(), off.size() * sizeof(int64_t))) != cudaSuccess)
+        return cuda_fail(e, "uploading CSC");
+    p->csc_uploaded = true;
+    return S2_OK;
+}
+
 int check_device(const s2_plan* p) {
     if (p->device < 0) return S2_OK;
     int cur = -1;

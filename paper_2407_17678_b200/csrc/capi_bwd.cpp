@@ -17,6 +17,13 @@ cudaError_t s2_launch_bwd_sm100(int which, int D, const CUtensorMap& q, const CU
                                 const void* fused_dout = nullptr, const float* fused_lse = nullptr,
                                 float* fused_delta = nullptr, float* fused_lse2 = nullptr);
 
+cudaError_t s2_launch_bwd_simt(bool bf16, const void* q, const void* k, const void* v, const void* out,
+                               const float* lse, const void* dout, void* dq, void* dk, void* dv,
+                               const int* bh_list, const int* head_of, int num_bh, const int* row_ptr,
+                               const int* col_idx, const int64_t* col_off, const int* col_ptr,
+                               const int* row_idx, const int64_t* row_off, float* delta, int N, int Npad,
+                               int D, int S, int B, int hpg, float scale, cudaStream_t stream);
+
 using namespace s2;
 
 namespace {
@@ -33,9 +40,11 @@ int check_bwd(const s2_plan* p, const s2_attn_bwd_args* a) {
     if (int rc = check_args(p, &a->fwd)) return rc;
     if (!a->dout || !a->dq || !a->dk || !a->dv)
         return fail(S2_ERR_INVALID_ARGUMENT, "dout/dq/dk/dv must be non-null device pointers");
-    if (!use_tcgen05(p, &a->fwd))
+    // shapes the tcgen05 kernels do not tile (fp32, other head_dim / block_size)
+    // run the fp32-FFMA tile kernels, which stage up to 128 columns
+    if (!use_tcgen05(p, &a->fwd) && a->fwd.head_dim > 128)
         return fail(S2_ERR_UNSUPPORTED,
-                    "backward needs bf16, head_dim in {64,128} and block_size % 16 == 0");
+                    "backward needs head_dim <= 128 (bf16 tcgen05: head_dim in {64,128}, block_size % 16 == 0)");
     return S2_OK;
 }
 }  // namespace
@@ -70,6 +79,17 @@ int s2_attn_bwd(s2_plan* p, const s2_attn_bwd_args* a, void* workspace, size_t w
     float* delta = static_cast<float*>(workspace);
     float* lse2 = delta + static_cast<size_t>(nqbh) * Npad;
     cudaError_t e = cudaSuccess;
+    if (!use_tcgen05(p, &f)) {
+        if ((rc = ensure_csr_uploaded(p)) || (rc = ensure_csc_uploaded(p))) return rc;
+        ProfScope prof("bwd_simt", st);
+        e = s2_launch_bwd_simt(f.dtype == S2_DTYPE_BF16, f.q, f.k, f.v, f.out, f.lse, a->dout, a->dq, a->dk,
+                               a->dv, w->simt_bh.as<int>(), w->simt_head.as<int>(), w->num_bh,
+                               p->d_row_ptr.as<int>(), p->d_col_idx.as<int>(), p->d_col_off.as<int64_t>(),
+                               p->d_col_ptr.as<int>(), p->d_row_idx.as<int>(), p->d_row_off.as<int64_t>(), delta,
+                               N, Npad, D, p->block_size, p->num_blocks, hpg, float(scale), st);
+        if (e != cudaSuccess) return cuda_fail(e, "s2_attn_bwd launch");
+        return S2_OK;
+    }
     // S2_PREP_FUSED=1 fuses the prep (Delta = rowsum(dO o O), lse2) into the dQ
     // kernel, which then runs first and leaves both in the workspace for dK/dV.  Off
     // by default: the per-item row loads of O and dO stall the elementwise warps at

@@ -30,6 +30,7 @@ inline double resolve_scale(double scale, int head_dim) {
 // pointers.
 int check_device(const s2_plan* p);
 int ensure_csr_uploaded(s2_plan* p);
+int ensure_csc_uploaded(s2_plan* p);
 Lists* get_lists(s2_plan* p, int seq_len, int* status);
 WorkItems* get_items(s2_plan* p, Lists* L, int batch, int num_units, const int* unit_ids,
                      int* status);

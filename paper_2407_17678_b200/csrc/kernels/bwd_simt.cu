@@ -1,0 +1,411 @@
+// S2-Attention backward, reference-precision path (fp32 arithmetic, FFMA).
+//
+// Serves the shapes the tcgen05 backward does not tile: S2_DTYPE_F32 (BASELINE
+// cfg1's precision, parity at 1e-4) and bf16 with head_dim not in {64, 128} or
+// block_size % 16 != 0, for head_dim <= 128.  The gradient is the one the oracle
+// restates (oracle/s2_oracle.c: s2o_attn_bwd) of the forward's admitted set
+// (/root/reference/proj/src/reference.cpp:28-36: the row block's CSR blocks, keys
+// <= the query position):
+//   P = exp(scale q.k - lse), Delta_i = dO_i . O_i, dS = P (dO.v - Delta),
+//   dQ = scale sum_j dS_ij k_j, dK = scale sum_i dS_ij q_i, dV = sum_i P_ij dO_i.
+// Three kernels, all in fixed visit orders with no atomics (deterministic):
+//   s2_bwd_simt_prep     Delta per row (one warp per row)
+//   s2_bwd_dq_tile       64 query rows x one query head per CTA, walking the row
+//                        block's CSR list (as the forward tile kernel does)
+//   s2_bwd_dkv_tile      64 keys x one kv head per CTA, walking the key block's CSC
+//                        list over every query head of the GQA group
+// The tile kernels use the forward tile kernel's 16 x 16 thread grid with 4 x 4
+// register blocks; operands of the score products are staged transposed
+// ([x][64], float4 reads), operands of the accumulating products row-major.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <stdint.h>
+
+#include <type_traits>
+
+namespace s2dev {
+namespace bsimt {
+
+template <typename T>
+__device__ __forceinline__ float ld(const T* p);
+template <>
+__device__ __forceinline__ float ld<float>(const float* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ float ld<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+template <typename T>
+__device__ __forceinline__ T cvt(float x);
+template <>
+__device__ __forceinline__ float cvt<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+
+struct Params {
+    const int* bh_list;      // [num_bh] data index of each query head (slot = unit * hpg + j)
+    const int* head_of;      // [num_bh] layout head
+    const int* row_ptr;      // [H][B+1] CSR
+    const int* col_idx;
+    const int64_t* col_off;  // [H]
+    const int* col_ptr;      // [H][B+1] CSC (key block -> query blocks)
+    const int* row_idx;
+    const int64_t* row_off;  // [H]
+    const float* lse;        // [bh][N], natural log (the forward's)
+    float* delta;            // [num_bh][Npad] workspace
+    int num_bh, N, Npad, D, S, B, hpg;
+    float scale;
+};
+
+// stage rows [row0, row0 + n) of a [N][D] head into smem, transposed ([x][64],
+// zero past n / D) and/or row-major ([64][DT])
+template <typename T, int DT>
+__device__ __forceinline__ void stage_t(float* dst, const T* src, int row0, int n, int D) {
+    for (int e = threadIdx.x; e < 64 * DT; e += 256) {
+        const int c = e & 63, x = e >> 6;
+        dst[x * 64 + c] = (c < n && x < D) ? ld(src + static_cast<size_t>(row0 + c) * D + x) : 0.f;
+    }
+}
+template <typename T, int DT>
+__device__ __forceinline__ void stage_r(float* dst, const T* src, int row0, int n, int D) {
+    for (int e = threadIdx.x; e < 64 * DT; e += 256) {
+        const int x = e % DT, c = e / DT;
+        dst[c * DT + x] = (c < n && x < D) ? ld(src + static_cast<size_t>(row0 + c) * D + x) : 0.f;
+    }
+}
+
+// Delta_i = sum_x dO_ix O_ix; 0 for rows without an admitted key (lse -inf, O NaN)
+template <typename T>
+__global__ void __launch_bounds__(256) s2_bwd_simt_prep(const T* __restrict__ out, const T* __restrict__ dout,
+                                                        const Params p) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * 8 + warp, slot = blockIdx.y;
+    if (row >= p.N) return;
+    const int bh = p.bh_list[slot];
+    const size_t base = (static_cast<size_t>(bh) * p.N + row) * p.D;
+    float acc = 0.f;
+    for (int x = lane; x < p.D; x += 32) acc = fmaf(ld(dout + base + x), ld(out + base + x), acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+        const bool live = p.lse[static_cast<size_t>(bh) * p.N + row] != -INFINITY;
+        p.delta[static_cast<size_t>(slot) * p.Npad + row] = live ? acc : 0.f;
+    }
+}
+
+// dQ: one CTA = 64 query rows (a 64-row sub-tile of one query block) x one query head
+template <typename T, int DT>
+__global__ void __launch_bounds__(256) s2_bwd_dq_tile(const T* __restrict__ q, const T* __restrict__ k,
+                                                      const T* __restrict__ v, const T* __restrict__ dout,
+                                                      T* __restrict__ dq, const Params p) {
+    constexpr int CW = DT / 16;
+    extern __shared__ __align__(16) float sm[];
+    float* Qt = sm;              // [DT][64]
+    float* dOt = Qt + DT * 64;   // [DT][64]
+    float* Kt = dOt + DT * 64;   // [DT][64]
+    float* Vt = Kt + DT * 64;    // [DT][64]
+    float* Ks = Vt + DT * 64;    // [64][DT]
+    float* dSs = Ks + 64 * DT;   // [64][68]
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int N = p.N, D = p.D, S = p.S;
+    const int nsub = (S + 63) >> 6;
+    const int xb = gridDim.x - 1 - blockIdx.x;  // late (long-row) query blocks first
+    const int qb = xb / nsub, sub = xb - qb * nsub;
+    const int slot = blockIdx.y;
+    const int bh = p.bh_list[slot], head = p.head_of[slot], kvbh = bh / p.hpg;
+    const int r0 = qb * S + sub * 64;
+    const int r_end = min(min(qb * S + S, N), r0 + 64);
+    if (r0 >= r_end) return;
+    const T* Q = q + static_cast<size_t>(bh) * N * D;
+    const T* dO = dout + static_cast<size_t>(bh) * N * D;
+    const T* K = k + static_cast<size_t>(kvbh) * N * D;
+    const T* V = v + static_cast<size_t>(kvbh) * N * D;
+    const int* rp = p.row_ptr + static_cast<size_t>(head) * (p.B + 1);
+    const int* ci = p.col_idx + p.col_off[head];
+
+    stage_t<T, DT>(Qt, Q, r0, r_end - r0, D);
+    stage_t<T, DT>(dOt, dO, r0, r_end - r0, D);
+    // P = exp2(scale log2e s - lse log2e); rows past the tile or without an admitted
+    // key get lse2 = +inf (P = 0) and Delta = 0
+    float lse2[4], dl[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = r0 + 4 * ty + i;
+        const float l = row < r_end ? p.lse[static_cast<size_t>(bh) * N + row] : -INFINITY;
+        lse2[i] = l == -INFINITY ? INFINITY : l * 1.4426950408889634f;
+        dl[i] = row < r_end ? p.delta[static_cast<size_t>(slot) * p.Npad + row] : 0.f;
+    }
+    const float sl2 = p.scale * 1.4426950408889634f;
+    float acc[4][CW];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < CW; ++j) acc[i][j] = 0.f;
+    const int row_last = r_end - 1;
+    for (int ptr = rp[qb]; ptr < rp[qb + 1]; ++ptr) {
+        const int kb0 = ci[ptr] * S;
+        const int kb_end = min(min(kb0 + S, N), row_last + 1);
+        for (int k0 = kb0; k0 < kb_end; k0 += 64) {
+            const int nk = min(64, kb_end - k0);
+            __syncthreads();  // the previous chunk's reads are done
+            stage_t<T, DT>(Kt, K, k0, nk, D);
+            stage_t<T, DT>(Vt, V, k0, nk, D);
+            stage_r<T, DT>(Ks, K, k0, nk, D);
+            __syncthreads();
+            float s[4][4], dp[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) s[i][j] = dp[i][j] = 0.f;
+#pragma unroll 2
+            for (int x = 0; x < D; ++x) {
+                const float4 a = *reinterpret_cast<const float4*>(Qt + x * 64 + 4 * ty);
+                const float4 b = *reinterpret_cast<const float4*>(Kt + x * 64 + 4 * tx);
+                const float4 c = *reinterpret_cast<const float4*>(dOt + x * 64 + 4 * ty);
+                const float4 d = *reinterpret_cast<const float4*>(Vt + x * 64 + 4 * tx);
+                const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+                const float cv[4] = {c.x, c.y, c.z, c.w}, dv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        s[i][j] = fmaf(av[i], bv[j], s[i][j]);
+                        dp[i][j] = fmaf(cv[i], dv[j], dp[i][j]);
+                    }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int row = r0 + 4 * ty + i;
+                float ds[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int key = k0 + 4 * tx + j;
+                    const bool ok = 4 * tx + j < nk && key <= row;
+                    const float pr = ok ? exp2f(fmaf(s[i][j], sl2, -lse2[i])) : 0.f;
+                    ds[j] = pr * (dp[i][j] - dl[i]);
+                }
+                *reinterpret_cast<float4*>(dSs + (4 * ty + i) * 68 + 4 * tx) = make_float4(ds[0], ds[1], ds[2], ds[3]);
+            }
+            __syncthreads();
+#pragma unroll 2
+            for (int c = 0; c < nk; ++c) {
+                float dv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dv[i] = dSs[(4 * ty + i) * 68 + c];
+#pragma unroll
+                for (int j4 = 0; j4 < CW; j4 += 4) {
+                    const float4 w = *reinterpret_cast<const float4*>(Ks + c * DT + tx * CW + j4);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        acc[i][j4 + 0] = fmaf(dv[i], w.x, acc[i][j4 + 0]);
+                        acc[i][j4 + 1] = fmaf(dv[i], w.y, acc[i][j4 + 1]);
+                        acc[i][j4 + 2] = fmaf(dv[i], w.z, acc[i][j4 + 2]);
+                        acc[i][j4 + 3] = fmaf(dv[i], w.w, acc[i][j4 + 3]);
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = r0 + 4 * ty + i;
+        if (row >= r_end) continue;
+        T* o = dq + static_cast<size_t>(bh) * N * D + static_cast<size_t>(row) * D;
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+            const int x = tx * CW + j;
+            if (x < D) o[x] = cvt<T>(acc[i][j] * p.scale);
+        }
+    }
+}
+
+// dK / dV: one CTA = 64 keys (a 64-key sub-tile of one key block) x one kv head; it
+// walks, for every query head of the group in order, the key block's CSC list
+// (ascending query blocks) in 64-row query chunks
+template <typename T, int DT>
+__global__ void __launch_bounds__(256) s2_bwd_dkv_tile(const T* __restrict__ q, const T* __restrict__ k,
+                                                       const T* __restrict__ v, const T* __restrict__ dout,
+                                                       T* __restrict__ dk, T* __restrict__ dv, const Params p) {
+    constexpr int CW = DT / 16;
+    extern __shared__ __align__(16) float sm[];
+    float* Kt = sm;              // [DT][64]
+    float* Vt = Kt + DT * 64;    // [DT][64]
+    float* Qt = Vt + DT * 64;    // [DT][64]
+    float* dOt = Qt + DT * 64;   // [DT][64]
+    float* Qs = dOt + DT * 64;   // [64][DT]
+    float* dOs = Qs + 64 * DT;   // [64][DT]
+    float* Ps = dOs + 64 * DT;   // [64][68]
+    float* dSs = Ps + 64 * 68;   // [64][68]
+    float* Ls = dSs + 64 * 68;   // [64] lse2 of the chunk's rows
+    float* Ds = Ls + 64;         // [64] Delta of the chunk's rows
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int N = p.N, D = p.D, S = p.S;
+    const int nsub = (S + 63) >> 6;
+    const int xb = blockIdx.x;
+    const int kb = xb / nsub, sub = xb - kb * nsub;
+    const int unit = blockIdx.y;
+    const int k0 = kb * S + sub * 64;
+    const int k_end = min(min(kb * S + S, N), k0 + 64);
+    if (k0 >= k_end) return;
+    const int kvbh = p.bh_list[unit * p.hpg] / p.hpg;
+    const T* K = k + static_cast<size_t>(kvbh) * N * D;
+    const T* V = v + static_cast<size_t>(kvbh) * N * D;
+    stage_t<T, DT>(Kt, K, k0, k_end - k0, D);
+    stage_t<T, DT>(Vt, V, k0, k_end - k0, D);
+    const float sl2 = p.scale * 1.4426950408889634f;
+    float ak[4][CW], av[4][CW];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < CW; ++j) ak[i][j] = av[i][j] = 0.f;
+    for (int hj = 0; hj < p.hpg; ++hj) {
+        const int slot = unit * p.hpg + hj;
+        const int bh = p.bh_list[slot], head = p.head_of[slot];
+        const T* Q = q + static_cast<size_t>(bh) * N * D;
+        const T* dO = dout + static_cast<size_t>(bh) * N * D;
+        const int* cp = p.col_ptr + static_cast<size_t>(head) * (p.B + 1);
+        const int* ri = p.row_idx + p.row_off[head];
+        for (int ptr = cp[kb]; ptr < cp[kb + 1]; ++ptr) {
+            const int qb = ri[ptr];
+            const int q_end = min(qb * S + S, N);
+            // rows before the tile's first key admit none of its keys
+            for (int r0 = max(qb * S, k0); r0 < q_end; r0 += 64) {
+                const int nq = min(64, q_end - r0);
+                __syncthreads();  // the previous chunk's reads are done
+                stage_t<T, DT>(Qt, Q, r0, nq, D);
+                stage_t<T, DT>(dOt, dO, r0, nq, D);
+                stage_r<T, DT>(Qs, Q, r0, nq, D);
+                stage_r<T, DT>(dOs, dO, r0, nq, D);
+                if (tid < 64) {
+                    const int row = r0 + tid;
+                    const float l = tid < nq ? p.lse[static_cast<size_t>(bh) * N + row] : -INFINITY;
+                    Ls[tid] = l == -INFINITY ? INFINITY : l * 1.4426950408889634f;
+                    Ds[tid] = tid < nq ? p.delta[static_cast<size_t>(slot) * p.Npad + row] : 0.f;
+                }
+                __syncthreads();
+                float s[4][4], dp[4][4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) s[i][j] = dp[i][j] = 0.f;
+#pragma unroll 2
+                for (int x = 0; x < D; ++x) {
+                    const float4 a = *reinterpret_cast<const float4*>(Kt + x * 64 + 4 * ty);
+                    const float4 b = *reinterpret_cast<const float4*>(Qt + x * 64 + 4 * tx);
+                    const float4 c = *reinterpret_cast<const float4*>(Vt + x * 64 + 4 * ty);
+                    const float4 d = *reinterpret_cast<const float4*>(dOt + x * 64 + 4 * tx);
+                    const float avv[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+                    const float cv[4] = {c.x, c.y, c.z, c.w}, dvv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            s[i][j] = fmaf(avv[i], bv[j], s[i][j]);
+                            dp[i][j] = fmaf(cv[i], dvv[j], dp[i][j]);
+                        }
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {  // S^T row: key 4ty+i; columns: query rows 4tx+j
+                    const int key = k0 + 4 * ty + i;
+                    float pr[4], ds[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int c = 4 * tx + j;
+                        const bool ok = key < k_end && c < nq && r0 + c >= key;
+                        pr[j] = ok ? exp2f(fmaf(s[i][j], sl2, -Ls[c])) : 0.f;
+                        ds[j] = pr[j] * (dp[i][j] - Ds[c]);
+                    }
+                    *reinterpret_cast<float4*>(Ps + (4 * ty + i) * 68 + 4 * tx) = make_float4(pr[0], pr[1], pr[2], pr[3]);
+                    *reinterpret_cast<float4*>(dSs + (4 * ty + i) * 68 + 4 * tx) = make_float4(ds[0], ds[1], ds[2], ds[3]);
+                }
+                __syncthreads();
+#pragma unroll 2
+                for (int c = 0; c < nq; ++c) {
+                    float pv[4], dsv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        pv[i] = Ps[(4 * ty + i) * 68 + c];
+                        dsv[i] = dSs[(4 * ty + i) * 68 + c];
+                    }
+#pragma unroll
+                    for (int j4 = 0; j4 < CW; j4 += 4) {
+                        const float4 wo = *reinterpret_cast<const float4*>(dOs + c * DT + tx * CW + j4);
+                        const float4 wq = *reinterpret_cast<const float4*>(Qs + c * DT + tx * CW + j4);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            av[i][j4 + 0] = fmaf(pv[i], wo.x, av[i][j4 + 0]);
+                            av[i][j4 + 1] = fmaf(pv[i], wo.y, av[i][j4 + 1]);
+                            av[i][j4 + 2] = fmaf(pv[i], wo.z, av[i][j4 + 2]);
+                            av[i][j4 + 3] = fmaf(pv[i], wo.w, av[i][j4 + 3]);
+                            ak[i][j4 + 0] = fmaf(dsv[i], wq.x, ak[i][j4 + 0]);
+                            ak[i][j4 + 1] = fmaf(dsv[i], wq.y, ak[i][j4 + 1]);
+                            ak[i][j4 + 2] = fmaf(dsv[i], wq.z, ak[i][j4 + 2]);
+                            ak[i][j4 + 3] = fmaf(dsv[i], wq.w, ak[i][j4 + 3]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    // every key of the tile is written: 0 for keys no query attends
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int key = k0 + 4 * ty + i;
+        if (key >= k_end) continue;
+        const size_t o = (static_cast<size_t>(kvbh) * N + key) * D;
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+            const int x = tx * CW + j;
+            if (x < D) {
+                dk[o + x] = cvt<T>(ak[i][j] * p.scale);
+                dv[o + x] = cvt<T>(av[i][j]);
+            }
+        }
+    }
+}
+
+}  // namespace bsimt
+}  // namespace s2dev
+
+// One backward over the plan's CSR / CSC (device arrays as s2_launch_fwd_simt's):
+// prep, dQ, dK/dV on `stream`.  bh_list / head_of: num_bh = num_units * hpg slots,
+// unit-major.  delta: [num_bh][Npad] floats of workspace.  head_dim <= 128.
+cudaError_t s2_launch_bwd_simt(bool bf16, const void* q, const void* k, const void* v, const void* out,
+                               const float* lse, const void* dout, void* dq, void* dk, void* dv,
+                               const int* bh_list, const int* head_of, int num_bh, const int* row_ptr,
+                               const int* col_idx, const int64_t* col_off, const int* col_ptr,
+                               const int* row_idx, const int64_t* row_off, float* delta, int N, int Npad,
+                               int D, int S, int B, int hpg, float scale, cudaStream_t stream) {
+    using namespace s2dev::bsimt;
+    if (num_bh == 0 || N == 0) return cudaSuccess;
+    if (D > 128) return cudaErrorInvalidValue;
+    const Params p{bh_list, head_of, row_ptr, col_idx, col_off, col_ptr, row_idx, row_off, lse, delta,
+                   num_bh, N, Npad, D, S, B, hpg, scale};
+    const int nsub = (S + 63) / 64;
+    auto run = [&](auto tag, auto dtag) -> cudaError_t {
+        constexpr int DT = decltype(dtag)::value;
+        using T = typename decltype(tag)::type;
+        const T* tq = static_cast<const T*>(q);
+        const T* tk = static_cast<const T*>(k);
+        const T* tv = static_cast<const T*>(v);
+        const T* to = static_cast<const T*>(out);
+        const T* tdo = static_cast<const T*>(dout);
+        s2_bwd_simt_prep<T><<<dim3((N + 7) / 8, num_bh), 256, 0, stream>>>(to, tdo, p);
+        const int smem_q = (5 * DT * 64 + 64 * 68) * 4;
+        const int smem_kv = (6 * DT * 64 + 2 * 64 * 68 + 128) * 4;
+        cudaError_t e;
+        if ((e = cudaFuncSetAttribute(s2_bwd_dq_tile<T, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q)) !=
+                cudaSuccess ||
+            (e = cudaFuncSetAttribute(s2_bwd_dkv_tile<T, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      smem_kv)) != cudaSuccess)
+            return e;
+        s2_bwd_dq_tile<T, DT><<<dim3(B * nsub, num_bh), 256, smem_q, stream>>>(tq, tk, tv, tdo, static_cast<T*>(dq),
+                                                                                p);
+        s2_bwd_dkv_tile<T, DT><<<dim3(B * nsub, num_bh / hpg), 256, smem_kv, stream>>>(
+            tq, tk, tv, tdo, static_cast<T*>(dk), static_cast<T*>(dv), p);
+        return cudaGetLastError();
+    };
+    struct F32 { using type = float; };
+    struct BF16 { using type = __nv_bfloat16; };
+    if (bf16)
+        return D <= 64 ? run(BF16{}, std::integral_constant<int, 64>{}) : run(BF16{}, std::integral_constant<int, 128>{});
+    return D <= 64 ? run(F32{}, std::integral_constant<int, 64>{}) : run(F32{}, std::integral_constant<int, 128>{});
+}

@@ -79,6 +79,9 @@ struct s2_plan {
     // device CSR (SIMT path)
     s2::DevBuf d_row_ptr, d_col_idx, d_col_off;
     bool csr_uploaded = false;
+    // device CSC (SIMT backward): key block -> query blocks, per head
+    s2::DevBuf d_col_ptr, d_row_idx, d_row_off;
+    bool csc_uploaded = false;
     std::mutex mu;
     int device = -1;  // CUDA device of the first call that built device-side state
     std::map<int, std::unique_ptr<s2::Lists>> lists;  // keyed by seq_len

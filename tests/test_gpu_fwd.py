@@ -324,6 +324,8 @@ def test_bf16_other_head_dims_take_the_simt_kernel_and_match_oracle(d):
     ro, rl = oracle.attn_fwd(q, k, v, rp, ci, 1, H, Hkv, N, d, S)
     np.testing.assert_allclose(out.float().cpu().numpy().ravel(), ro, rtol=1e-2, atol=1e-2)
     np.testing.assert_allclose(lse.cpu().numpy().ravel(), rl, rtol=1e-2, atol=1e-2)
-    # no backward for these shapes: an explicit error, never a silent fallback
-    with pytest.raises(s2.S2Unsupported):
-        s2.s2_attn_bwd(s2.Plan.from_config(cfg), T(q, H), T(k, Hkv), T(v, Hkv), out, lse, out)
+    # head_dim > 128 has no backward: an explicit error, never a silent fallback
+    # (head_dim <= 128 runs the fp32-FFMA backward: tests/test_gpu_bwd_simt.py)
+    if d > 128:
+        with pytest.raises(s2.S2Unsupported):
+            s2.s2_attn_bwd(s2.Plan.from_config(cfg), T(q, H), T(k, Hkv), T(v, Hkv), out, lse, out)
