@@ -5,7 +5,7 @@
     compute-sanitizer --tool synccheck python tools/sanitize_run.py
 
 It covers the bf16 tcgen05 forward and backward (D = 64 / 128, MHA and GQA, a ragged
-N, batch 2, a tile with no keys), the fp32 forwards (tiled and row-wise), the CTA-pair forward when S2_FWD_2CTA=1,
+N, batch 2, a tile with no keys), the fp32 forwards (tiled and row-wise) and the fp32-FFMA backward, the CTA-pair forward when S2_FWD_2CTA=1,
 the layout / compaction /
 append kernels and the split-KV decode with its combine.  Results are not checked here:
 the parity tests do that.  The process exits non-zero if a CUDA call fails.
@@ -50,9 +50,20 @@ def main():
     for N, S, D in ((300, 32, 64), (333, 128, 17), (200, 16, 300)):
         plan = s2.Plan.from_config(s2.make_s2_config(N, 2, block_size=S, local_blocks=2, vert_stride=2))
         x = [rnd(1, 2, N, D, dt=torch.float32, g=g) for _ in range(3)]
-        s2.s2_attn_fwd(plan, *x)
+        out, lse = s2.s2_attn_fwd(plan, *x)
+        if D <= 128:  # the fp32-FFMA backward (bwd_simt.cu)
+            s2.s2_attn_bwd(plan, *x, out, lse, rnd(1, 2, N, D, dt=torch.float32, g=g))
         torch.cuda.synchronize()
-        print(f"fp32 fwd N={N} block={S} D={D}: ok", flush=True)
+        print(f"fp32 fwd{'+bwd' if D <= 128 else ''} N={N} block={S} D={D}: ok", flush=True)
+    # the FFMA backward with GQA, batch 2 and bf16 at an untiled head dim
+    plan = s2.Plan.from_config(s2.make_s2_config(500, 4, block_size=48, local_blocks=2, vert_stride=3,
+                                                 num_kv_heads=2))
+    q, do = rnd(2, 4, 500, 96, g=g), rnd(2, 4, 500, 96, g=g)
+    k, vv = rnd(2, 2, 500, 96, g=g), rnd(2, 2, 500, 96, g=g)
+    out, lse = s2.s2_attn_fwd(plan, q, k, vv)
+    s2.s2_attn_bwd(plan, q, k, vv, out, lse, do)
+    torch.cuda.synchronize()
+    print("bf16 D=96 block 48 GQA batch 2 fwd+bwd (FFMA kernels): ok", flush=True)
     # the opt-in CTA-pair forward (fwd_pair2.cu)
     if os.environ.get("S2_FWD_2CTA") == "1":
         plan = s2.Plan.from_config(s2.make_s2_config(1000, 4, block_size=64, local_blocks=2, vert_stride=3))
