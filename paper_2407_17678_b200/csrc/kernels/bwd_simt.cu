@@ -77,7 +77,9 @@ template <typename T>
 __global__ void __launch_bounds__(256) s2_bwd_simt_prep(const T* __restrict__ out, const T* __restrict__ dout,
                                                         const Params p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int row = blockIdx.x * 8 + warp, slot = blockIdx.y;
+    // flat 1-D grid (no 65535 cap on batch x heads)
+    const int row = static_cast<int>(blockIdx.x / p.num_bh) * 8 + warp;
+    const int slot = static_cast<int>(blockIdx.x % p.num_bh);
     if (row >= p.N) return;
     const int bh = p.bh_list[slot];
     const size_t base = (static_cast<size_t>(bh) * p.N + row) * p.D;
@@ -107,9 +109,10 @@ __global__ void __launch_bounds__(256) s2_bwd_dq_tile(const T* __restrict__ q, c
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int N = p.N, D = p.D, S = p.S;
     const int nsub = (S + 63) >> 6;
-    const int xb = gridDim.x - 1 - blockIdx.x;  // late (long-row) query blocks first
+    // flat 1-D grid (no 65535 cap on batch x heads): late (long-row) query blocks first
+    const int xb = p.B * nsub - 1 - static_cast<int>(blockIdx.x / p.num_bh);
     const int qb = xb / nsub, sub = xb - qb * nsub;
-    const int slot = blockIdx.y;
+    const int slot = static_cast<int>(blockIdx.x % p.num_bh);
     const int bh = p.bh_list[slot], head = p.head_of[slot], kvbh = bh / p.hpg;
     const int r0 = qb * S + sub * 64;
     const int r_end = min(min(qb * S + S, N), r0 + 64);
@@ -239,9 +242,11 @@ __global__ void __launch_bounds__(256) s2_bwd_dkv_tile(const T* __restrict__ q, 
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int N = p.N, D = p.D, S = p.S;
     const int nsub = (S + 63) >> 6;
-    const int xb = blockIdx.x;
+    // flat 1-D grid: early key blocks (the longest transposed lists) first
+    const int nunits = p.num_bh / p.hpg;
+    const int xb = static_cast<int>(blockIdx.x / nunits);
     const int kb = xb / nsub, sub = xb - kb * nsub;
-    const int unit = blockIdx.y;
+    const int unit = static_cast<int>(blockIdx.x % nunits);
     const int k0 = kb * S + sub * 64;
     const int k_end = min(min(kb * S + S, N), k0 + 64);
     if (k0 >= k_end) return;
@@ -388,7 +393,7 @@ cudaError_t s2_launch_bwd_simt(bool bf16, const void* q, const void* k, const vo
         const T* tv = static_cast<const T*>(v);
         const T* to = static_cast<const T*>(out);
         const T* tdo = static_cast<const T*>(dout);
-        s2_bwd_simt_prep<T><<<dim3((N + 7) / 8, num_bh), 256, 0, stream>>>(to, tdo, p);
+        s2_bwd_simt_prep<T><<<dim3(static_cast<unsigned>((N + 7) / 8) * num_bh), 256, 0, stream>>>(to, tdo, p);
         const int smem_q = (5 * DT * 64 + 64 * 68) * 4;
         const int smem_kv = (6 * DT * 64 + 2 * 64 * 68 + 128) * 4;
         cudaError_t e;
@@ -397,9 +402,9 @@ cudaError_t s2_launch_bwd_simt(bool bf16, const void* q, const void* k, const vo
             (e = cudaFuncSetAttribute(s2_bwd_dkv_tile<T, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       smem_kv)) != cudaSuccess)
             return e;
-        s2_bwd_dq_tile<T, DT><<<dim3(B * nsub, num_bh), 256, smem_q, stream>>>(tq, tk, tv, tdo, static_cast<T*>(dq),
+        s2_bwd_dq_tile<T, DT><<<dim3(static_cast<unsigned>(B) * nsub * num_bh), 256, smem_q, stream>>>(tq, tk, tv, tdo, static_cast<T*>(dq),
                                                                                 p);
-        s2_bwd_dkv_tile<T, DT><<<dim3(B * nsub, num_bh / hpg), 256, smem_kv, stream>>>(
+        s2_bwd_dkv_tile<T, DT><<<dim3(static_cast<unsigned>(B) * nsub * (num_bh / hpg)), 256, smem_kv, stream>>>(
             tq, tk, tv, tdo, static_cast<T*>(dk), static_cast<T*>(dv), p);
         return cudaGetLastError();
     };

@@ -57,8 +57,9 @@ __global__ void __launch_bounds__(128) s2_fwd_simt_kernel(const T* __restrict__ 
                                                           const SimtParams p) {
     extern __shared__ float sq[];  // [4 warps][D]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qb = blockIdx.x;
-    const int slot = blockIdx.y;
+    // flat 1-D grid (no 65535 cap on batch x heads): late (long-row) blocks first
+    const int qb = p.B - 1 - static_cast<int>(blockIdx.x / p.num_bh);
+    const int slot = static_cast<int>(blockIdx.x % p.num_bh);
     const int bh = p.bh_list[slot];
     const int head = p.head_of[slot];
     const int kvbh = bh / p.hpg;
@@ -155,9 +156,10 @@ __global__ void __launch_bounds__(256) s2_fwd_tile_kernel(const T* __restrict__ 
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int N = p.N, D = p.D, S = p.S;
     const int nsub = (S + 63) >> 6;
-    const int xb = gridDim.x - 1 - blockIdx.x;  // late (long-row) query blocks first
+    // flat 1-D grid (no 65535 cap on batch x heads): late (long-row) query blocks first
+    const int xb = p.B * nsub - 1 - static_cast<int>(blockIdx.x / p.num_bh);
     const int qb = xb / nsub, sub = xb - qb * nsub;
-    const int slot = blockIdx.y;
+    const int slot = static_cast<int>(blockIdx.x % p.num_bh);
     const int bh = p.bh_list[slot], head = p.head_of[slot], kvbh = bh / p.hpg;
     const int r0 = qb * S + sub * 64;
     const int r_end = min(min(qb * S + S, N), r0 + 64);
@@ -292,7 +294,7 @@ cudaError_t s2_launch_fwd_simt(bool bf16, const void* q, const void* k, const vo
     s2dev::SimtParams p{bh_list, head_of, row_ptr, col_idx, col_off, num_bh, N, D, S, B, hpg, scale};
     if (D <= 256 && std::getenv("S2_SIMT_ROWWISE") == nullptr) {
         // tiled kernel: 64-row sub-tiles of every query block
-        dim3 grid(B * ((S + 63) / 64), num_bh);
+        const dim3 grid(static_cast<unsigned>(B) * ((S + 63) / 64) * num_bh);
         auto launch = [&](auto tag) {
             constexpr int DT = decltype(tag)::value;
             const size_t smem = (3 * DT * 64 + 64 * 68) * sizeof(float);
@@ -317,7 +319,7 @@ cudaError_t s2_launch_fwd_simt(bool bf16, const void* q, const void* k, const vo
         return cudaGetLastError();
     }
     // row-wise kernel: head_dim up to 2048 (S2_SIMT_ROWWISE=1 forces it for any D)
-    dim3 grid(B, num_bh);
+    const dim3 grid(static_cast<unsigned>(B) * num_bh);
     const size_t smem = 4 * D * sizeof(float);  // <= 32 KB
     auto launch = [&](auto tag) {
         constexpr int DPL = decltype(tag)::value;
