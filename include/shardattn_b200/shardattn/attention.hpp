@@ -5,7 +5,7 @@
 //   naive_masked_attention / dense_masked_attention -> the same kernel after
 //     the reference's mask validation (dense: finiteness + causal masks)
 // Extensions in the house style (the reference has neither):
-//   streaming_sharded_attention_backward -> tcgen05 bf16 backward kernels
+//   streaming_sharded_attention_backward -> fp32 sm_100a backward kernels
 //   sharded_decode -> compacted KV cache + split-KV decode kernel
 #pragma once
 
@@ -47,8 +47,9 @@ void streaming_sharded_attention(AttentionTensors& t, const std::vector<CsrMask>
 void dsplit_attention(AttentionTensors& t, const std::vector<CsrMask>& csr, int block_size,
                       int num_splits);
 
-/// Gradients of sum(dout * out) w.r.t. q, k, v for the forward above (inputs
-/// rounded to bf16, tensor-core kernels; tolerance 1e-2).  Shapes as q/k/v.
+/// Gradients of sum(dout * out) w.r.t. q, k, v for the forward above, in fp32
+/// like the forward (tolerance 1e-4 against an fp64 restatement); head_dim <= 128
+/// (larger throws std::invalid_argument).  Shapes as q/k/v.
 struct AttentionGrads {
     std::vector<float> dq, dk, dv;
 };

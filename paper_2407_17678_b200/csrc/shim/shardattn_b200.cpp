@@ -395,33 +395,18 @@ void streaming_sharded_attention_backward(const AttentionTensors& t,
     for (const CsrMask& c : csr) c.validate();
     const size_t n = t.q.size();
     if (dout.size() != n) throw std::invalid_argument("dout size does not match [heads, seq, dim]");
-    auto to_bf16 = [](const std::vector<float>& x) {
-        std::vector<uint16_t> r(x.size());
-        for (size_t i = 0; i < x.size(); ++i) {
-            uint32_t u;
-            std::memcpy(&u, &x[i], 4);
-            r[i] = static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
-        }
-        return r;
-    };
-    auto from_bf16 = [](const std::vector<uint16_t>& x) {
-        std::vector<float> r(x.size());
-        for (size_t i = 0; i < x.size(); ++i) {
-            const uint32_t u = static_cast<uint32_t>(x[i]) << 16;
-            std::memcpy(&r[i], &u, 4);
-        }
-        return r;
-    };
+    if (t.head_dim > 128) throw std::invalid_argument("backward supports head_dim <= 128");
+    // fp32 end to end, like the forward: the reference-precision backward kernels
+    // (bwd_simt.cu; head_dim <= 128, else S2_ERR_UNSUPPORTED -> invalid_argument)
     Plan plan = make_plan(csr, t.seq_len, block_size);
     const size_t rows = static_cast<size_t>(t.num_heads) * t.seq_len;
-    Dev q(n * 2), k(n * 2), v(n * 2), o(n * 2), l(rows * 4), g(n * 2), dq(n * 2), dk(n * 2), dv(n * 2);
-    const auto hq = to_bf16(t.q), hk = to_bf16(t.k), hv = to_bf16(t.v), hg = to_bf16(dout);
-    ck(s2_memcpy_h2d(q.p, hq.data(), n * 2, nullptr));
-    ck(s2_memcpy_h2d(k.p, hk.data(), n * 2, nullptr));
-    ck(s2_memcpy_h2d(v.p, hv.data(), n * 2, nullptr));
-    ck(s2_memcpy_h2d(g.p, hg.data(), n * 2, nullptr));
+    Dev q(n * 4), k(n * 4), v(n * 4), o(n * 4), l(rows * 4), g(n * 4), dq(n * 4), dk(n * 4), dv(n * 4);
+    ck(s2_memcpy_h2d(q.p, t.q.data(), n * 4, nullptr));
+    ck(s2_memcpy_h2d(k.p, t.k.data(), n * 4, nullptr));
+    ck(s2_memcpy_h2d(v.p, t.v.data(), n * 4, nullptr));
+    ck(s2_memcpy_h2d(g.p, dout.data(), n * 4, nullptr));
     s2_attn_bwd_args a{};
-    a.fwd.dtype = S2_DTYPE_BF16;
+    a.fwd.dtype = S2_DTYPE_F32;
     a.fwd.batch = 1;
     a.fwd.num_heads = t.num_heads;
     a.fwd.num_kv_heads = t.num_heads;
@@ -443,16 +428,13 @@ void streaming_sharded_attention_backward(const AttentionTensors& t,
     ck(s2_attn_bwd_workspace_size(plan.p, &a, &ws));
     Dev w(ws);
     ck(s2_attn_bwd(plan.p, &a, w.p, ws, nullptr));
-    std::vector<uint16_t> r(n);
-    ck(s2_memcpy_d2h(r.data(), dq.p, n * 2, nullptr));
+    grads.dq.resize(n);
+    grads.dk.resize(n);
+    grads.dv.resize(n);
+    ck(s2_memcpy_d2h(grads.dq.data(), dq.p, n * 4, nullptr));
+    ck(s2_memcpy_d2h(grads.dk.data(), dk.p, n * 4, nullptr));
+    ck(s2_memcpy_d2h(grads.dv.data(), dv.p, n * 4, nullptr));
     ck(s2_stream_synchronize(nullptr));
-    grads.dq = from_bf16(r);
-    ck(s2_memcpy_d2h(r.data(), dk.p, n * 2, nullptr));
-    ck(s2_stream_synchronize(nullptr));
-    grads.dk = from_bf16(r);
-    ck(s2_memcpy_d2h(r.data(), dv.p, n * 2, nullptr));
-    ck(s2_stream_synchronize(nullptr));
-    grads.dv = from_bf16(r);
 }
 
 void sharded_decode(AttentionTensors& t, const std::vector<CsrMask>& csr, int block_size, int position) {

@@ -2,6 +2,7 @@
 // backed by the B200 kernels, exercised the way /root/reference/proj/tests use it.
 // Restates test_attention.cpp:72-294 and test_csr.cpp:30-42; the comparison
 // oracle is the C restatement (oracle/s2_oracle.c, linked here as test infra).
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -198,26 +199,32 @@ int main() {
         naive_masked_attention(a, in.masks, 8);
         CHECK(close(a.out, ro, 1e-4));
     }
-    // extension: backward on tensor cores vs the fp64 oracle (bf16 tolerance)
-    {
-        Inst in = make(2, 300, 64, 64, 2, 7, 2);
+    // extension: backward (fp32, like the forward) vs the fp64 oracle at 1e-4, at a
+    // tensor-core shape and at an odd one (block 24, head_dim 40)
+    for (const auto& [H, N, D, S] : {std::array<int, 4>{2, 300, 64, 64}, std::array<int, 4>{3, 250, 40, 24}}) {
+        Inst in = make(H, N, D, S, 2, 7, 2);
         std::vector<float> dout(in.t.q.size());
         std::mt19937_64 g(5);
         std::uniform_real_distribution<float> u(-1.f, 1.f);
         for (float& x : dout) x = u(g);
         AttentionGrads gr;
-        streaming_sharded_attention_backward(in.t, in.csr, 64, dout, gr);
+        streaming_sharded_attention_backward(in.t, in.csr, S, dout, gr);
         std::vector<int> rp, ci;
         for (const CsrMask& c : in.csr) {
             rp.insert(rp.end(), c.row_ptr.begin(), c.row_ptr.end());
             ci.insert(ci.end(), c.col_idx.begin(), c.col_idx.end());
         }
         std::vector<float> dq(dout.size()), dk(dout.size()), dv(dout.size());
-        s2o_attn_bwd(1, 2, 2, 300, 64, 64, in.t.scale, in.t.q.data(), in.t.k.data(), in.t.v.data(),
+        s2o_attn_bwd(1, H, H, N, D, S, in.t.scale, in.t.q.data(), in.t.k.data(), in.t.v.data(),
                      dout.data(), rp.data(), ci.data(), dq.data(), dk.data(), dv.data());
-        CHECK(close(gr.dq, dq, 2e-2));
-        CHECK(close(gr.dk, dk, 2e-2));
-        CHECK(close(gr.dv, dv, 2e-2));
+        CHECK(close(gr.dq, dq, 1e-4));
+        CHECK(close(gr.dk, dk, 1e-4));
+        CHECK(close(gr.dv, dv, 1e-4));
+    }
+    {  // head_dim > 128 has no backward: the reference's exception type
+        Inst in = make(1, 100, 160, 64, 1, 3, 2);
+        AttentionGrads gr;
+        CHECK_THROWS(streaming_sharded_attention_backward(in.t, in.csr, 64, std::vector<float>(in.t.q.size()), gr));
     }
     // extension: decode of one position over the compacted cache == that row of the
     // forward (bf16 operands: 2e-2), rows <= position only; other rows zero / -inf
