@@ -122,3 +122,42 @@ def test_head_dim_over_128_bwd_is_unsupported():
     out, lse = s2.s2_attn_fwd(plan, x, x, x)
     with pytest.raises(s2.S2Unsupported):
         s2.s2_attn_bwd(plan, x, x, x, out, lse, x)
+
+
+def test_f32_autograd_op_matches_torch_fp64_autograd():
+    """s2_attention (torch.library op) on fp32 tensors: forward and the gradients of
+    a random loss against torch fp64 autograd of the dense masked softmax built from
+    the same block layout (the token mask of reference.cpp:28-36), at 1e-4."""
+    import torch
+
+    from paper_2407_17678_b200.torch_ops import s2_attention
+
+    cfg = single(320, 32, 2, 2, 3)
+    H, N, D, S = 2, 320, 48, 32
+    rp, ci = oracle.csr_all(cfg)
+    B = (N + S - 1) // S
+    mask = np.zeros((H, N, N), bool)
+    off = 0
+    for h in range(H):
+        r = rp[h * (B + 1):(h + 1) * (B + 1)] if len(rp) == H * (B + 1) else None
+        assert r is not None
+        for qb in range(B):
+            for e in range(r[qb], r[qb + 1]):
+                kb = ci[off + e]
+                mask[h, qb * S:(qb + 1) * S, kb * S:(kb + 1) * S] = True
+        off += r[B]
+    mask &= np.tril(np.ones((N, N), bool))[None]
+    g = torch.Generator().manual_seed(11)
+    q, k, v, do = (torch.rand(1, H, N, D, generator=g, dtype=torch.float64) * 2 - 1 for _ in range(4))
+    qc, kc, vc = (x.float().cuda().requires_grad_() for x in (q, k, v))
+    out = s2_attention(qc, kc, vc, s2.Plan.from_config(cfg))
+    out.backward(do.float().cuda())
+    qr, kr, vr = (x.clone().requires_grad_() for x in (q, k, v))
+    sc = (qr @ kr.transpose(-1, -2)) / np.sqrt(D)
+    sc = sc.masked_fill(~torch.from_numpy(mask)[None], float("-inf"))
+    ref = torch.softmax(sc, -1) @ vr
+    ref.backward(do)
+    tol = dict(rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(out.detach().cpu().double(), ref.detach(), **tol)
+    for got, want in ((qc.grad, qr.grad), (kc.grad, kr.grad), (vc.grad, vr.grad)):
+        torch.testing.assert_close(got.cpu().double(), want, **tol)
