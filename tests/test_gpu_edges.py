@@ -81,12 +81,13 @@ def test_short_and_ragged_sequences_match_oracle(N, S, local, vs):
         np.testing.assert_allclose(f(g_), r_, rtol=1e-2, atol=1e-2)
 
 
-def test_unattended_value_rows_change_nothing_fwd_and_bwd():
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_unattended_value_rows_change_nothing_fwd_and_bwd(dt):
     """A hand-made CSR whose key blocks 5..7 no row attends (rows 5..7 list only
     block 0, every other row {0, i}): V rows there perturbed by +1000 change no
     output, lse or gradient; their dK / dV rows are exactly 0 (no tile covers
     those chunks: the backward zero-fills them -- found by this test when the
-    output buffers held stale data)."""
+    output buffers held stale data).  f32: the FFMA forward and backward."""
     import torch
 
     from paper_2407_17678_b200.pattern import CsrMask
@@ -98,7 +99,8 @@ def test_unattended_value_rows_change_nothing_fwd_and_bwd():
     ci = np.concatenate(rows).astype(np.int32)
     plan = s2.Plan.from_csr([CsrMask(h, B, rp, ci) for h in range(H)], N, S)
     g = torch.Generator(device="cuda").manual_seed(3)
-    mk = lambda: (torch.rand(1, H, N, 128, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)  # noqa
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    mk = lambda: (torch.rand(1, H, N, 128, device="cuda", generator=g) * 2 - 1).to(tdt)  # noqa
     q, k, v, do = mk(), mk(), mk(), mk()
     v2 = v.clone()
     v2[:, :, 5 * S:8 * S] += 1000
@@ -112,7 +114,8 @@ def test_unattended_value_rows_change_nothing_fwd_and_bwd():
     assert torch.all(dv[:, :, 5 * S:8 * S] == 0) and torch.all(dk[:, :, 5 * S:8 * S] == 0)
 
 
-def test_rows_without_keys_follow_the_reference():
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_rows_without_keys_follow_the_reference(dt):
     """A CSR row block that lists no key block: the reference yields out = 0/0 = NaN
     and lse = -inf for its rows (acc / l with nothing admitted); so do the kernels,
     whether the 128-row tile has other attended rows or none at all."""
@@ -128,24 +131,27 @@ def test_rows_without_keys_follow_the_reference():
     plan = s2.Plan.from_csr([CsrMask(h, B, rp, ci) for h in range(H)], N, S)
     rng = np.random.default_rng(4)
     q, k, v = (bf16_round(rng.uniform(-1, 1, H * N * D).astype(np.float32)) for _ in range(3))
-    out, lse = s2.s2_attn_fwd(plan, *(_t(x, (1, H, N, D)) for x in (q, k, v)))
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    tol = dict(rtol=1e-2, atol=1e-2) if dt == "bf16" else dict(rtol=1e-4, atol=1e-4)
+    tt = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.float32)).reshape(1, H, N, D).to("cuda", tdt)  # noqa
+    out, lse = s2.s2_attn_fwd(plan, *(tt(x) for x in (q, k, v)))
     torch.cuda.synchronize()
     ro, rl = oracle.attn_fwd(q, k, v, np.tile(rp, H), np.tile(ci, H), 1, H, H, N, D, S)
     o = out.float().cpu().numpy().ravel()
-    np.testing.assert_allclose(o, ro, rtol=1e-2, atol=1e-2, equal_nan=True)
-    np.testing.assert_allclose(lse.cpu().numpy().ravel(), rl, rtol=1e-2, atol=1e-2, equal_nan=True)
+    np.testing.assert_allclose(o, ro, **tol, equal_nan=True)
+    np.testing.assert_allclose(lse.cpu().numpy().ravel(), rl, **tol, equal_nan=True)
     assert np.isnan(ro).any() and np.array_equal(np.isnan(o), np.isnan(ro))
     # backward: those rows admit no key, so they contribute nothing (dQ rows 0,
     # no dK / dV terms) even though their lse is -inf and their O is NaN
     do = bf16_round(rng.uniform(-1, 1, H * N * D).astype(np.float32))
-    tq, tk, tv, tdo = (_t(x, (1, H, N, D)) for x in (q, k, v, do))
+    tq, tk, tv, tdo = (tt(x) for x in (q, k, v, do))
     dq, dk, dv = s2.s2_attn_bwd(plan, tq, tk, tv, out, lse, tdo)
     torch.cuda.synchronize()
     rq, rk, rv = oracle.attn_bwd(q, k, v, do, np.tile(rp, H), np.tile(ci, H), 1, H, H, N, D, S)
     for g_, r_ in ((dq, rq), (dk, rk), (dv, rv)):
         gg = g_.float().cpu().numpy().ravel()
         assert np.isfinite(gg).all()
-        np.testing.assert_allclose(gg, r_, rtol=1e-2, atol=1e-2)
+        np.testing.assert_allclose(gg, r_, **tol)
 
 
 def test_tensor_contract_errors_raise_instead_of_reading_out_of_bounds():
