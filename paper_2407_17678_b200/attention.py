@@ -269,7 +269,10 @@ def s2_attn_fwd_peers(plan: Plan, q, k, v, *, unit_ids, peer_out, peer_lse, unit
 
 def s2_attn_bwd(plan: Plan, q, k, v, out, lse, dout, *, scale: Optional[float] = None,
                 dq=None, dk=None, dv=None, unit_ids=None, stream=None):
-    """Sparse backward: (dq, dk, dv).  dK/dV tiles are owned by one CTA each (no atomics)."""
+    """Sparse backward: (dq, dk, dv).  dK/dV tiles are owned by one CTA each (no atomics).
+    bf16 with head_dim 64 / 128 and block_size % 16 == 0 -> tcgen05 kernels; fp32 (and
+    other bf16 shapes) with head_dim <= 128 -> reference-precision FFMA kernels;
+    head_dim > 128 otherwise raises S2Unsupported."""
     import torch
 
     _require_cuda(q, k, v, out, lse, dout)
