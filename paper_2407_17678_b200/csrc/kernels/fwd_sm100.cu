@@ -97,15 +97,18 @@ struct Fwd2Cfg {
     static constexpr int kQBytes = kSub * 16384;  // 128 rows
     static constexpr int kCBytes = kSub * 8192;   // one 64-key chunk of K (or V)
 // exp2 on the FMA pipe (cubic) for 1 in (mask+1) pairs; -1: all on MUFU.EX2.
-// With separate S / P V issuers the MUFU pipe no longer paces the softmax, and
-// emulation only adds instructions (same-box A/B: 25% 0.784 ms, 12.5% 0.760 ms,
-// 0% 0.748 ms).
+// The two tiles' softmax warps on one SM sub-partition share its MUFU (4 lanes per
+// cycle); a small share on the FMA pipe shortens their exponential phases, a
+// large one only adds instructions.  Same-box A/B (r2g): 1 in 16 0.677 vs 0.683 ms
+// and 0.715 vs 0.727; 1 in 8 0.678-0.680; 1 in 4 0.688.  (Making the two warps take
+// turns on the MUFU instead lost: 0.78 ms.)
 #ifndef S2_FWD_POLY_MASK
-#define S2_FWD_POLY_MASK -1
+#define S2_FWD_POLY_MASK 15
 #endif
 #ifndef S2_FWD_NST
 #define S2_FWD_NST 4
 #endif
+
     static constexpr int kNST = D == 128 ? S2_FWD_NST : 8;
     static constexpr int kStageBytes = 2 * kCBytes;
     // per tile, a 128-row x 64-column bf16 staging slice for the O epilogue's TMA stores
@@ -391,6 +394,7 @@ __global__ void __launch_bounds__(384, 1)
                         tmem_ld32(tS + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
                         tmem_ld_wait();
                     }
+                    if (r == 0 && t == 0) S2FTRACE(16, s_cnt - 1);
                     apply_mask(sv, chunk, msk, rg, q_pos, row0);
                     float mxa[8];
 #pragma unroll
@@ -412,6 +416,7 @@ __global__ void __launch_bounds__(384, 1)
                             rescale = true;
                         }
                     }
+                    if (r == 0 && t == 0) S2FTRACE(17, s_cnt - 1);
                     if (__any_sync(0xffffffffu, rescale)) {
                         // O must hold every earlier chunk's P V before it is rescaled: the
                         // last one issued is this tile's chunk k_here-1 (its (k_here-1)-th
@@ -461,6 +466,7 @@ __global__ void __launch_bounds__(384, 1)
                         f2_unpack(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), a0, a1);
                         l_run += a0 + a1;
                     }
+                    if (r == 0 && t == 0) S2FTRACE(18, s_cnt - 1);
                     tmem_st_wait();
                     tc_fence_before();
                     mbar_arrive(smem_u32(&bar_pf[t][half]));

@@ -82,3 +82,15 @@ if nk > 40:
     print(f"  slow chunks: wait K {np.median(wk[idx]):.0f}, S issue incl. half waits {np.median(iss[idx]):.0f}, "
           f"gap to next {np.median(gap[idx]):.0f}  (all chunks: {np.median(wk[:nk]):.0f} / {np.median(iss[:nk]):.0f} / "
           f"{np.median(gap[:nk - 1]):.0f})")
+
+# softmax phases of tile 0 (slots 16-18 between S ready (5) and P arrive (8))
+if (t[16] > 0).sum() > 40:
+    a, b = 20, min(int((t[16] > 0).sum()), 1500)
+    ph = {"S ready -> TMEM ld done": t[16, a:b] - t[5, a:b],
+          "mask + max + rescale test": t[17, a:b] - t[16, a:b],
+          "rescale + exp + P st issue": t[18, a:b] - t[17, a:b],
+          "st wait + fence + arrive": t[8, a:b] - t[18, a:b],
+          "arrive -> next S wait start": t[4, a + 1:b + 1] - t[8, a:b],
+          "wait S": t[5, a + 1:b + 1] - t[4, a + 1:b + 1]}
+    for k_, v_ in ph.items():
+        print(f"  softmax0 {k_}: median {np.median(v_):.0f}, mean {np.mean(v_):.0f}")
