@@ -447,6 +447,11 @@ __global__ void __launch_bounds__(384, 1)
                         for (int j = 0; j < 16; ++j) {
                             const uint64_t x = ffma2(f2_pack(sv[c * 32 + 2 * j], sv[c * 32 + 2 * j + 1]), sl2v, nbase);
                             uint64_t pr;
+#ifdef S2_FWD_ABLATE_EXP  // timing experiments only (wrong results): no exponentials
+                            if (true) {
+                                pr = x;
+                            } else
+#endif
                             if (S2_FWD_POLY_MASK >= 0 && (j & S2_FWD_POLY_MASK) == S2_FWD_POLY_MASK) {  // 1 in (mask+1) on the FMA pipe
                                 pr = exp2_poly2(x);
                             } else {
