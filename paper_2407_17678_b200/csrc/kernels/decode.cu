@@ -92,6 +92,11 @@ __global__ void __launch_bounds__(160) s2_decode_split_kernel(const __grid_const
         fence_mbar_init();
     }
     __syncthreads();
+    // programmatic dependent launch: the combine's CTAs may be scheduled from here;
+    // q, the cache and o_part / lse_part (read by the previous combine) are only
+    // touched after the previous kernel in the stream has completed
+    pdl_launch_dependents();
+    pdl_wait();
 
     if (warp == 4) {
         // ---------------------------------------------------------- producer
@@ -240,6 +245,7 @@ __global__ void s2_decode_combine_kernel(const float* __restrict__ o_part,
                                          const float* __restrict__ lse_part, int splits, int D,
                                          __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
     const int bh = blockIdx.x;
+    pdl_wait();  // the split kernel's partials are complete and visible
     const float* lp = lse_part + static_cast<size_t>(bh) * splits;
     float m = -INFINITY;
     for (int s = 0; s < splits; ++s) m = fmaxf(m, lp[s]);
@@ -306,8 +312,7 @@ static cudaError_t launch_decode(const CUtensorMap& mk, const CUtensorMap& mv,
     auto kern = s2_decode_split_kernel<HPG, D>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<dim3(p.splits, p.Hkv, batch), 160, smem, st>>>(mk, mv, p);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(p.splits, p.Hkv, batch), dim3(160), smem, st, mk, mv, p);
 }
 
 cudaError_t s2_launch_decode(const CUtensorMap& mk, const CUtensorMap& mv, const DecodeParams& p,
@@ -322,8 +327,8 @@ cudaError_t s2_launch_decode(const CUtensorMap& mk, const CUtensorMap& mv, const
 
 cudaError_t s2_launch_decode_combine(const float* o_part, const float* lse_part, int splits, int D,
                                      int num_bh, __nv_bfloat16* out, float* lse, cudaStream_t st) {
-    s2_decode_combine_kernel<<<num_bh, 128, 0, st>>>(o_part, lse_part, splits, D, out, lse);
-    return cudaGetLastError();
+    return launch_pdl(s2_decode_combine_kernel, dim3(num_bh), dim3(128), 0, st, o_part, lse_part, splits, D, out,
+                      lse);
 }
 
 cudaError_t s2_launch_kv_compact(const void* k, const void* v, void* kp, void* vp,
