@@ -11,18 +11,22 @@ from helpers import single
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("case", ["s2", "gqa_batch2"])
+@pytest.mark.parametrize("case", ["s2", "gqa_batch2", "f32_ffma"])
 def test_fwd_bwd_step_captures_into_a_cuda_graph(case):
     import torch
 
+    dt, D = torch.bfloat16, 128
     if case == "s2":
         cfg, B, H, Hkv = single(2048, 64, 4, 2, 4), 1, 4, 4
-    else:
+    elif case == "gqa_batch2":
         cfg, B, H, Hkv = single(1024, 64, 8, 2, 4, kv=2), 2, 8, 2
+    else:  # the fp32-FFMA forward and backward (CSC uploaded by the warm-up call)
+        cfg, B, H, Hkv = single(700, 48, 4, 2, 3, kv=2), 2, 4, 2
+        dt, D = torch.float32, 64
     plan = s2.Plan.from_config(cfg)
-    N, D = cfg.seq_len, 128
+    N = cfg.seq_len
     g = torch.Generator(device="cuda").manual_seed(11)
-    mk = lambda h: (torch.rand(B, h, N, D, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)  # noqa
+    mk = lambda h: (torch.rand(B, h, N, D, device="cuda", generator=g) * 2 - 1).to(dt)  # noqa
     q, k, v, do = mk(H), mk(Hkv), mk(Hkv), mk(H)
     out, lse = torch.empty_like(q), torch.empty(B, H, N, device="cuda")
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
