@@ -161,3 +161,40 @@ def test_f32_autograd_op_matches_torch_fp64_autograd():
     torch.testing.assert_close(out.detach().cpu().double(), ref.detach(), **tol)
     for got, want in ((qc.grad, qr.grad), (kc.grad, kr.grad), (vc.grad, vr.grad)):
         torch.testing.assert_close(got.cpu().double(), want, **tol)
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("N", [1, 2, 7, 65])
+def test_tiny_sequences_fwd_bwd(dt, N):
+    """N below one block (test_attention.cpp:72-79,149-156's N=1 and N<S cases) through
+    the forward and backward: N=1 gives out = v exactly, dq = dk = 0 and dv = dout up
+    to rounding."""
+    import torch
+
+    H, D, S = 2, 64 if dt == "f32" else 128, 64
+    cfg = single(N, S, H, 1, 1) if N <= S else single(N, S, H, 1, 2)
+    tdt = torch.float32 if dt == "f32" else torch.bfloat16
+    tol = dict(rtol=1e-4, atol=1e-4) if dt == "f32" else dict(rtol=1e-2, atol=1e-2)
+    rng = np.random.default_rng(N)
+    q, k, v, do = (rng.uniform(-1, 1, H * N * D).astype(np.float32) for _ in range(4))
+    if dt == "bf16":
+        q, k, v, do = (bf16_round(x) for x in (q, k, v, do))
+    T = lambda x: torch.from_numpy(x).reshape(1, H, N, D).to("cuda", tdt)  # noqa: E731
+    plan = s2.Plan.from_config(cfg)
+    tq, tk, tv, tdo = T(q), T(k), T(v), T(do)
+    out, lse = s2.s2_attn_fwd(plan, tq, tk, tv)
+    dq, dk, dv = s2.s2_attn_bwd(plan, tq, tk, tv, out, lse, tdo)
+    torch.cuda.synchronize()
+    rp, ci = oracle.csr_all(cfg)
+    ro, _ = oracle.attn_fwd(q, k, v, rp, ci, 1, H, H, N, D, S)
+    ref = oracle.attn_bwd(q, k, v, do, rp, ci, 1, H, H, N, D, S)
+    f = lambda t: t.float().cpu().numpy().ravel()  # noqa: E731
+    np.testing.assert_allclose(f(out), ro, **tol)
+    for nm, g_, r_ in zip(("dq", "dk", "dv"), (dq, dk, dv), ref):
+        np.testing.assert_allclose(f(g_), np.ravel(r_), **tol, err_msg=nm)
+    if N == 1:  # one admitted key: P = 1, so out = v exactly (the reference's pin);
+        # dS = dP - Delta vanishes up to rounding, dv = dout up to the rounding of P
+        assert torch.equal(out, tv)
+        small = 1e-6 if dt == "f32" else 1e-2
+        assert dq.float().abs().max() <= small and dk.float().abs().max() <= small
+        torch.testing.assert_close(dv.float(), tdo.float(), **tol)
