@@ -35,7 +35,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cfg, batch, D, res_path):
+def _worker(rank, world, port, cfg, batch, D, res_path, f32=False):
     import torch
     import torch.distributed as dist
 
@@ -49,7 +49,8 @@ def _worker(rank, world, port, cfg, batch, D, res_path):
     plan = s2.Plan.from_config(cfg)
     N, H, Hkv = cfg.seq_len, cfg.num_heads, cfg.kv_heads()
     g = torch.Generator(device="cuda").manual_seed(7)
-    mk = lambda h: (torch.rand((batch, h, N, D), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)  # noqa
+    dt = torch.float32 if f32 else torch.bfloat16
+    mk = lambda h: (torch.rand((batch, h, N, D), device="cuda", generator=g) * 2 - 1).to(dt)  # noqa
     q, k, v, do = mk(H), mk(Hkv), mk(Hkv), mk(H)
     hp = HeadParallelPlan(plan, batch, world)
     out, lse = head_parallel_forward(plan, q, k, v, rank, world, hp=hp)
@@ -76,16 +77,19 @@ def _worker(rank, world, port, cfg, batch, D, res_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["mha_b2", "gqa"])
+@pytest.mark.parametrize("case", ["mha_b2", "gqa", "f32_gqa_b2"])
 def test_head_parallel_world2_on_one_gpu_is_bit_identical(case, tmp_path):
     import torch.multiprocessing as mp
 
+    f32 = False
     if case == "mha_b2":
         cfg, batch, D = single(1024, 64, 4, 2, 4), 2, 128
-    else:
+    elif case == "gqa":
         cfg, batch, D = single(2048, 64, 8, 4, 4, kv=2), 1, 128
+    else:  # the fp32-FFMA forward and backward on each rank's units
+        cfg, batch, D, f32 = single(640, 32, 8, 3, 3, kv=4), 2, 64, True
     res = str(tmp_path / "res.txt")
-    mp.spawn(_worker, args=(2, _free_port(), cfg, batch, D, res), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), cfg, batch, D, res, f32), nprocs=2, join=True)
     assert open(res).read() == "ok"
 
 
