@@ -24,6 +24,8 @@
 
 #include <type_traits>
 
+#include "sm100_ptx.cuh"
+
 namespace s2dev {
 namespace bsimt {
 
@@ -222,8 +224,13 @@ __global__ void __launch_bounds__(256) s2_bwd_dq_tile(const T* __restrict__ q, c
 
 // dK / dV: one CTA = 64 keys (a 64-key sub-tile of one key block) x one kv head; it
 // walks, for every query head of the group in order, the key block's CSC list
-// (ascending query blocks) in 64-row query chunks
-template <typename T, int DT>
+// (ascending query blocks) in 64-row query chunks.  SPLIT = 2: a cluster of two CTAs
+// shares the tile -- CTA rank r takes the chunks with (chunk index % 2) == r -- and
+// rank 0 adds rank 1's accumulators (read through distributed shared memory) to its
+// own before the store: a fixed order, so still deterministic.  A stripe key block,
+// which every later query block attends, has a list up to B long while a local-only
+// one has a few entries; splitting halves the longest CTA.
+template <typename T, int DT, int SPLIT>
 __global__ void __launch_bounds__(256) s2_bwd_dkv_tile(const T* __restrict__ q, const T* __restrict__ k,
                                                        const T* __restrict__ v, const T* __restrict__ dout,
                                                        T* __restrict__ dk, T* __restrict__ dv, const Params p) {
@@ -244,12 +251,14 @@ __global__ void __launch_bounds__(256) s2_bwd_dkv_tile(const T* __restrict__ q, 
     const int nsub = (S + 63) >> 6;
     // flat 1-D grid: early key blocks (the longest transposed lists) first
     const int nunits = p.num_bh / p.hpg;
-    const int xb = static_cast<int>(blockIdx.x / nunits);
+    const int crank = SPLIT > 1 ? static_cast<int>(blockIdx.x % SPLIT) : 0;  // cluster rank (1-D clusters)
+    const int cid = static_cast<int>(blockIdx.x / SPLIT);
+    const int xb = cid / nunits;
     const int kb = xb / nsub, sub = xb - kb * nsub;
-    const int unit = static_cast<int>(blockIdx.x % nunits);
+    const int unit = cid % nunits;
     const int k0 = kb * S + sub * 64;
     const int k_end = min(min(kb * S + S, N), k0 + 64);
-    if (k0 >= k_end) return;
+    if (k0 >= k_end) return;  // (uniform across the cluster: both ranks share the tile)
     const int kvbh = p.bh_list[unit * p.hpg] / p.hpg;
     const T* K = k + static_cast<size_t>(kvbh) * N * D;
     const T* V = v + static_cast<size_t>(kvbh) * N * D;
@@ -261,6 +270,7 @@ __global__ void __launch_bounds__(256) s2_bwd_dkv_tile(const T* __restrict__ q, 
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < CW; ++j) ak[i][j] = av[i][j] = 0.f;
+    int qc = 0;  // query chunk index over the whole walk (SPLIT: this rank's share)
     for (int hj = 0; hj < p.hpg; ++hj) {
         const int slot = unit * p.hpg + hj;
         const int bh = p.bh_list[slot], head = p.head_of[slot];
@@ -273,6 +283,7 @@ __global__ void __launch_bounds__(256) s2_bwd_dkv_tile(const T* __restrict__ q, 
             const int q_end = min(qb * S + S, N);
             // rows before the tile's first key admit none of its keys
             for (int r0 = max(qb * S, k0); r0 < q_end; r0 += 64) {
+                if (SPLIT > 1 && (qc++ % SPLIT) != crank) continue;
                 const int nq = min(64, q_end - r0);
                 __syncthreads();  // the previous chunk's reads are done
                 stage_t<T, DT>(Qt, Q, r0, nq, D);
@@ -350,6 +361,41 @@ __global__ void __launch_bounds__(256) s2_bwd_dkv_tile(const T* __restrict__ q, 
             }
         }
     }
+    if (SPLIT > 1) {
+        // ranks > 0 park their accumulators in their shared memory (thread-private
+        // slots); rank 0 adds them in, rank by rank, after the cluster barrier and stores
+        __syncthreads();
+        float* park = sm + static_cast<size_t>(tid) * (8 * CW);
+        if (crank != 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < CW; ++j) {
+                    park[i * CW + j] = ak[i][j];
+                    park[4 * CW + i * CW + j] = av[i][j];
+                }
+        }
+        s2dev::cluster_sync();
+        if (crank == 0) {
+            for (int rr = 1; rr < SPLIT; ++rr) {  // ranks in order: a fixed summation order
+                const uint32_t remote = s2dev::mapa_shared(s2dev::smem_u32(park), rr);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < CW; ++j) {
+                        float a, b;
+                        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(a) : "r"(remote + 4u * (i * CW + j)));
+                        asm volatile("ld.shared::cluster.f32 %0, [%1];"
+                                     : "=f"(b)
+                                     : "r"(remote + 4u * (4 * CW + i * CW + j)));
+                        ak[i][j] += a;
+                        av[i][j] += b;
+                    }
+            }
+        }
+        s2dev::cluster_sync();  // rank 1's shared memory outlives rank 0's reads
+        if (crank != 0) return;
+    }
     // every key of the tile is written: 0 for keys no query attends
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -369,6 +415,14 @@ __global__ void __launch_bounds__(256) s2_bwd_dkv_tile(const T* __restrict__ q, 
 
 }  // namespace bsimt
 }  // namespace s2dev
+
+// query-chunk split of the dK/dV tiles over a cluster (1: none).  A/B at cfg1's shape
+// (fp32, N=2048, H=8, D=64): backward 0.684 ms (1), 0.454 (2), 0.600 (4), 1.43 (8);
+// N=8192 D=128: 6.54 / 5.33 / 7.00 / 13.9 ms
+#ifndef S2_SIMT_DKV_SPLIT
+#define S2_SIMT_DKV_SPLIT 2
+#endif
+static constexpr int kDkvSplit = S2_SIMT_DKV_SPLIT;
 
 // One backward over the plan's CSR / CSC (device arrays as s2_launch_fwd_simt's):
 // prep, dQ, dK/dV on `stream`.  bh_list / head_of: num_bh = num_units * hpg slots,
@@ -397,15 +451,28 @@ cudaError_t s2_launch_bwd_simt(bool bf16, const void* q, const void* k, const vo
         const int smem_q = (5 * DT * 64 + 64 * 68) * 4;
         const int smem_kv = (6 * DT * 64 + 2 * 64 * 68 + 128) * 4;
         cudaError_t e;
+        auto dkv = s2_bwd_dkv_tile<T, DT, kDkvSplit>;
         if ((e = cudaFuncSetAttribute(s2_bwd_dq_tile<T, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q)) !=
                 cudaSuccess ||
-            (e = cudaFuncSetAttribute(s2_bwd_dkv_tile<T, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      smem_kv)) != cudaSuccess)
+            (e = cudaFuncSetAttribute(dkv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv)) != cudaSuccess)
             return e;
         s2_bwd_dq_tile<T, DT><<<dim3(static_cast<unsigned>(B) * nsub * num_bh), 256, smem_q, stream>>>(tq, tk, tv, tdo, static_cast<T*>(dq),
                                                                                 p);
-        s2_bwd_dkv_tile<T, DT><<<dim3(static_cast<unsigned>(B) * nsub * (num_bh / hpg)), 256, smem_kv, stream>>>(
-            tq, tk, tv, tdo, static_cast<T*>(dk), static_cast<T*>(dv), p);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(B) * nsub * (num_bh / hpg) * kDkvSplit);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem_kv;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kDkvSplit;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if ((e = cudaLaunchKernelEx(&cfg, dkv, tq, tk, tv, tdo, static_cast<T*>(dk), static_cast<T*>(dv), p)) !=
+            cudaSuccess)
+            return e;
         return cudaGetLastError();
     };
     struct F32 { using type = float; };
