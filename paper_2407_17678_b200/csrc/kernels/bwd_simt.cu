@@ -95,8 +95,51 @@ __global__ void __launch_bounds__(256) s2_bwd_simt_prep(const T* __restrict__ ou
     }
 }
 
-// dQ: one CTA = 64 query rows (a 64-row sub-tile of one query block) x one query head
-template <typename T, int DT>
+// Cluster reduction of per-thread accumulators (the SPLIT > 1 kernels): ranks > 0
+// park theirs in thread-private shared-memory slots, rank 0 adds them rank by rank
+// (a fixed order: deterministic).  Returns whether this CTA stores the result.
+template <int SPLIT, int CW>
+__device__ __forceinline__ bool cluster_sum(float (&a)[4][CW], float (&b)[4][CW], float* sm, bool two) {
+    if (SPLIT == 1) return true;
+    const int crank = static_cast<int>(blockIdx.x % SPLIT);
+    __syncthreads();  // the staging buffers are free
+    float* park = sm + static_cast<size_t>(threadIdx.x) * (8 * CW);
+    if (crank != 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < CW; ++j) {
+                park[i * CW + j] = a[i][j];
+                if (two) park[4 * CW + i * CW + j] = b[i][j];
+            }
+    }
+    s2dev::cluster_sync();
+    if (crank == 0) {
+        for (int rr = 1; rr < SPLIT; ++rr) {
+            const uint32_t remote = s2dev::mapa_shared(s2dev::smem_u32(park), rr);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < CW; ++j) {
+                    float x, y = 0.f;
+                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(remote + 4u * (i * CW + j)));
+                    if (two)
+                        asm volatile("ld.shared::cluster.f32 %0, [%1];"
+                                     : "=f"(y)
+                                     : "r"(remote + 4u * (4 * CW + i * CW + j)));
+                    a[i][j] += x;
+                    b[i][j] += y;
+                }
+        }
+    }
+    s2dev::cluster_sync();  // the parked slots outlive rank 0's reads
+    return crank == 0;
+}
+
+// dQ: one CTA = 64 query rows (a 64-row sub-tile of one query block) x one query
+// head.  SPLIT > 1: a cluster shares the tile, rank r taking key chunks with
+// (chunk index % SPLIT) == r, summed into rank 0 by cluster_sum.
+template <typename T, int DT, int SPLIT>
 __global__ void __launch_bounds__(256) s2_bwd_dq_tile(const T* __restrict__ q, const T* __restrict__ k,
                                                       const T* __restrict__ v, const T* __restrict__ dout,
                                                       T* __restrict__ dq, const Params p) {
@@ -112,13 +155,15 @@ __global__ void __launch_bounds__(256) s2_bwd_dq_tile(const T* __restrict__ q, c
     const int N = p.N, D = p.D, S = p.S;
     const int nsub = (S + 63) >> 6;
     // flat 1-D grid (no 65535 cap on batch x heads): late (long-row) query blocks first
-    const int xb = p.B * nsub - 1 - static_cast<int>(blockIdx.x / p.num_bh);
+    const int crank = SPLIT > 1 ? static_cast<int>(blockIdx.x % SPLIT) : 0;
+    const int cid = static_cast<int>(blockIdx.x / SPLIT);
+    const int xb = p.B * nsub - 1 - cid / p.num_bh;
     const int qb = xb / nsub, sub = xb - qb * nsub;
-    const int slot = static_cast<int>(blockIdx.x % p.num_bh);
+    const int slot = cid % p.num_bh;
     const int bh = p.bh_list[slot], head = p.head_of[slot], kvbh = bh / p.hpg;
     const int r0 = qb * S + sub * 64;
     const int r_end = min(min(qb * S + S, N), r0 + 64);
-    if (r0 >= r_end) return;
+    if (r0 >= r_end) return;  // (uniform across the cluster)
     const T* Q = q + static_cast<size_t>(bh) * N * D;
     const T* dO = dout + static_cast<size_t>(bh) * N * D;
     const T* K = k + static_cast<size_t>(kvbh) * N * D;
@@ -145,10 +190,12 @@ __global__ void __launch_bounds__(256) s2_bwd_dq_tile(const T* __restrict__ q, c
 #pragma unroll
         for (int j = 0; j < CW; ++j) acc[i][j] = 0.f;
     const int row_last = r_end - 1;
+    int kc = 0;  // key chunk index over the walk (SPLIT: this rank's share)
     for (int ptr = rp[qb]; ptr < rp[qb + 1]; ++ptr) {
         const int kb0 = ci[ptr] * S;
         const int kb_end = min(min(kb0 + S, N), row_last + 1);
         for (int k0 = kb0; k0 < kb_end; k0 += 64) {
+            if (SPLIT > 1 && (kc++ % SPLIT) != crank) continue;
             const int nk = min(64, kb_end - k0);
             __syncthreads();  // the previous chunk's reads are done
             stage_t<T, DT>(Kt, K, k0, nk, D);
@@ -209,6 +256,7 @@ __global__ void __launch_bounds__(256) s2_bwd_dq_tile(const T* __restrict__ q, c
             }
         }
     }
+    if (!cluster_sum<SPLIT, CW>(acc, acc, sm, false)) return;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int row = r0 + 4 * ty + i;
@@ -361,41 +409,7 @@ __global__ void __launch_bounds__(256) s2_bwd_dkv_tile(const T* __restrict__ q, 
             }
         }
     }
-    if (SPLIT > 1) {
-        // ranks > 0 park their accumulators in their shared memory (thread-private
-        // slots); rank 0 adds them in, rank by rank, after the cluster barrier and stores
-        __syncthreads();
-        float* park = sm + static_cast<size_t>(tid) * (8 * CW);
-        if (crank != 0) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < CW; ++j) {
-                    park[i * CW + j] = ak[i][j];
-                    park[4 * CW + i * CW + j] = av[i][j];
-                }
-        }
-        s2dev::cluster_sync();
-        if (crank == 0) {
-            for (int rr = 1; rr < SPLIT; ++rr) {  // ranks in order: a fixed summation order
-                const uint32_t remote = s2dev::mapa_shared(s2dev::smem_u32(park), rr);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < CW; ++j) {
-                        float a, b;
-                        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(a) : "r"(remote + 4u * (i * CW + j)));
-                        asm volatile("ld.shared::cluster.f32 %0, [%1];"
-                                     : "=f"(b)
-                                     : "r"(remote + 4u * (4 * CW + i * CW + j)));
-                        ak[i][j] += a;
-                        av[i][j] += b;
-                    }
-            }
-        }
-        s2dev::cluster_sync();  // rank 1's shared memory outlives rank 0's reads
-        if (crank != 0) return;
-    }
+    if (!cluster_sum<SPLIT, CW>(ak, av, sm, true)) return;
     // every key of the tile is written: 0 for keys no query attends
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -423,6 +437,12 @@ __global__ void __launch_bounds__(256) s2_bwd_dkv_tile(const T* __restrict__ q, 
 #define S2_SIMT_DKV_SPLIT 2
 #endif
 static constexpr int kDkvSplit = S2_SIMT_DKV_SPLIT;
+// dQ: the same split over key chunks does not pay (cfg1 shape 0.462 vs 0.453 ms,
+// N=8192 D=128 5.64 vs 5.33 ms): a query block's list is at most local + stripe long
+#ifndef S2_SIMT_DQ_SPLIT
+#define S2_SIMT_DQ_SPLIT 1
+#endif
+static constexpr int kDqSplit = S2_SIMT_DQ_SPLIT;
 
 // One backward over the plan's CSR / CSC (device arrays as s2_launch_fwd_simt's):
 // prep, dQ, dK/dV on `stream`.  bh_list / head_of: num_bh = num_units * hpg slots,
@@ -451,27 +471,31 @@ cudaError_t s2_launch_bwd_simt(bool bf16, const void* q, const void* k, const vo
         const int smem_q = (5 * DT * 64 + 64 * 68) * 4;
         const int smem_kv = (6 * DT * 64 + 2 * 64 * 68 + 128) * 4;
         cudaError_t e;
+        auto dqk = s2_bwd_dq_tile<T, DT, kDqSplit>;
         auto dkv = s2_bwd_dkv_tile<T, DT, kDkvSplit>;
-        if ((e = cudaFuncSetAttribute(s2_bwd_dq_tile<T, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q)) !=
-                cudaSuccess ||
+        if ((e = cudaFuncSetAttribute(dqk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q)) != cudaSuccess ||
             (e = cudaFuncSetAttribute(dkv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv)) != cudaSuccess)
             return e;
-        s2_bwd_dq_tile<T, DT><<<dim3(static_cast<unsigned>(B) * nsub * num_bh), 256, smem_q, stream>>>(tq, tk, tv, tdo, static_cast<T*>(dq),
-                                                                                p);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(static_cast<unsigned>(B) * nsub * (num_bh / hpg) * kDkvSplit);
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = smem_kv;
-        cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = kDkvSplit;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        if ((e = cudaLaunchKernelEx(&cfg, dkv, tq, tk, tv, tdo, static_cast<T*>(dk), static_cast<T*>(dv), p)) !=
-            cudaSuccess)
+        // both tile kernels in 1-D clusters of kDqSplit / kDkvSplit CTAs
+        auto cluster_launch = [&](auto kern, unsigned ctas, int split, int smem, auto... args) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(ctas * split);
+            cfg.blockDim = dim3(256);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = split;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            return cudaLaunchKernelEx(&cfg, kern, args...);
+        };
+        if ((e = cluster_launch(dqk, static_cast<unsigned>(B) * nsub * num_bh, kDqSplit, smem_q, tq, tk, tv, tdo,
+                                static_cast<T*>(dq), p)) != cudaSuccess ||
+            (e = cluster_launch(dkv, static_cast<unsigned>(B) * nsub * (num_bh / hpg), kDkvSplit, smem_kv, tq, tk, tv,
+                                tdo, static_cast<T*>(dk), static_cast<T*>(dv), p)) != cudaSuccess)
             return e;
         return cudaGetLastError();
     };
