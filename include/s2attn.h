@@ -236,8 +236,9 @@ int s2_attn_bwd(s2_plan* plan, const s2_attn_bwd_args* args, void* workspace,
 
 /* ---- one layer's forward + backward on HOST buffers -------------------------
  * The reference's data path (AttentionTensors in host memory, attention.hpp:
- * 17-37) for bf16: every pointer in `args` (q, k, v, dout in; out, lse, dq, dk,
- * dv out) is HOST memory, ideally pinned.  The (batch, kv-group) units are cut
+ * 17-37), for the shapes s2_attn_bwd takes (bf16 or fp32): every pointer in
+ * `args` (q, k, v, dout in; out, lse, dq, dk, dv out) is HOST memory, ideally
+ * pinned.  The (batch, kv-group) units are cut
  * into num_chunks chunks whose H2D copy, forward + backward and D2H copy are
  * pipelined on three streams (heads are independent, test_attention.cpp:
  * 217-240), so the PCIe transfers overlap each other and the kernels.

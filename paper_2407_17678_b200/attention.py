@@ -297,7 +297,7 @@ def s2_attn_fwd_bwd_host(plan: Plan, q, k, v, dout, out, lse, dq, dk, dv, *,
                          scale: Optional[float] = None, num_chunks: int = 4, stream=None,
                          workspace=None):
     """One layer's forward + backward on HOST tensors (pinned CPU torch tensors,
-    bf16; lse fp32): the reference API's host-resident data path.  The C ABI
+    bf16 or fp32; lse fp32): the reference API's host-resident data path.  The C ABI
     pipelines H2D copies, kernels and D2H copies over `num_chunks` chunks of
     (batch, kv-group) units (s2_attn_fwd_bwd_host).  Returns when the work is
     queued on `stream`; synchronize before reading the outputs."""

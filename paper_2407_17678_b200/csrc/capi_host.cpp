@@ -55,8 +55,9 @@ Layout layout(const s2_plan* p, const s2_attn_args& f) {
     const int hpg = p->num_heads / p->num_kv_heads;
     const size_t units = static_cast<size_t>(f.batch) * p->num_kv_heads;
     Layout L{};
-    L.q = static_cast<size_t>(hpg) * f.seq_len * f.head_dim * 2;
-    L.kv = static_cast<size_t>(f.seq_len) * f.head_dim * 2;
+    const size_t es = f.dtype == S2_DTYPE_F32 ? 4 : 2;  // element bytes
+    L.q = static_cast<size_t>(hpg) * f.seq_len * f.head_dim * es;
+    L.kv = static_cast<size_t>(f.seq_len) * f.head_dim * es;
     L.lse = static_cast<size_t>(hpg) * f.seq_len * 4;
     const size_t per[9] = {L.q, L.kv, L.kv, L.q, L.q, L.lse, L.q, L.kv, L.kv};
     size_t o = 0;
@@ -75,8 +76,10 @@ int check_host(const s2_plan* p, const s2_attn_bwd_args* a, int num_chunks) {
     if (int rc = check_args(p, &a->fwd)) return rc;
     if (!a->dout || !a->dq || !a->dk || !a->dv)
         return fail(S2_ERR_INVALID_ARGUMENT, "dout/dq/dk/dv must be non-null host pointers");
-    if (!use_tcgen05(p, &a->fwd))
-        return fail(S2_ERR_UNSUPPORTED, "the host path needs bf16, head_dim in {64,128} and block_size % 16 == 0");
+    // the shapes s2_attn_bwd takes: bf16 tcgen05 ones, and any fp32 / bf16 with
+    // head_dim <= 128 on the FFMA kernels
+    if (!use_tcgen05(p, &a->fwd) && a->fwd.head_dim > 128)
+        return fail(S2_ERR_UNSUPPORTED, "the host path needs head_dim <= 128 (the backward's limit)");
     return S2_OK;
 }
 

@@ -125,16 +125,20 @@ def test_hybrid_layer_stack_fwd_bwd():
             np.testing.assert_allclose(f(g), r, **TOL)
 
 
-def test_host_buffer_pipeline_matches_device_path():
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_host_buffer_pipeline_matches_device_path(dt):
     """s2_attn_fwd_bwd_host (host tensors, chunked H2D / kernels / D2H on three
-    streams) returns exactly what the device path returns."""
+    streams) returns exactly what the device path returns -- on the tcgen05 kernels
+    (bf16) and on the FFMA kernels (fp32, the reference API's precision)."""
     import torch
 
-    cfg = single(2048, 64, 8, 4, 8, kv=4)
+    if dt == "bf16":
+        cfg, B, H, Hkv, N, D, tdt = single(2048, 64, 8, 4, 8, kv=4), 2, 8, 4, 2048, 128, torch.bfloat16
+    else:
+        cfg, B, H, Hkv, N, D, tdt = single(640, 32, 4, 3, 4, kv=2), 2, 4, 2, 640, 64, torch.float32
     plan = s2.Plan.from_config(cfg)
-    B, H, Hkv, N, D = 2, 8, 4, 2048, 128
     g = torch.Generator().manual_seed(9)
-    mk = lambda h: (torch.rand((B, h, N, D), generator=g) * 2 - 1).to(torch.bfloat16).pin_memory()  # noqa
+    mk = lambda h: (torch.rand((B, h, N, D), generator=g) * 2 - 1).to(tdt).pin_memory()  # noqa
     q, k, v, do = mk(H), mk(Hkv), mk(Hkv), mk(H)
     outs = [torch.empty_like(q).pin_memory(), torch.empty((B, H, N), dtype=torch.float32).pin_memory(),
             torch.empty_like(q).pin_memory(), torch.empty_like(k).pin_memory(), torch.empty_like(v).pin_memory()]
