@@ -35,6 +35,10 @@ namespace s2dev {
 // Delta = rowsum(dO o O) and lse*log2(e) per row; HBM-bound (reads O and dO
 // once).  D/8 lanes own a row (16-byte loads), 256 / (D/8) rows per 256-thread
 // block iteration, grid-stride over rows.
+#ifndef S2_DKV_L2HINT
+#define S2_DKV_L2HINT 1
+#endif
+
 template <int D>
 __global__ void __launch_bounds__(256) s2_bwd_prep_kernel(const __nv_bfloat16* __restrict__ out,
                                                           const __nv_bfloat16* __restrict__ dout,
@@ -252,6 +256,9 @@ __global__ void __launch_bounds__(384, 1)
             tma_prefetch(&tmK);
             tma_prefetch(&tmV);
             uint32_t it_cnt = 0, st_it = 0;
+            // S2_DKV_L2HINT: Q / dO rows are re-streamed by every key tile of the head
+            // (keep them in L2); a key tile's K / V are read once (stream them)
+            const uint64_t keep = policy_evict_last(), once = policy_evict_first();
             for (int i = i_beg; i < i_end; ++i, ++it_cnt) {
                 const BwdItem it = items[i];
                 const int kb = it_cnt & 1;
@@ -262,13 +269,19 @@ __global__ void __launch_bounds__(384, 1)
                 for (int h = 0; h < nc; ++h)
                     for (int s = 0; s < C::kSub; ++s) {
                         const int row = (h ? it.c1 : it.c0) * 64;
-                        tma_load_3d(sK + kvoff + s * 16384 + h * 8192, &tmK, kvbar, s * 64, row, it.kvbh);
+                        if (S2_DKV_L2HINT)
+                            tma_load_3d_hint(sK + kvoff + s * 16384 + h * 8192, &tmK, kvbar, s * 64, row, it.kvbh, once);
+                        else
+                            tma_load_3d(sK + kvoff + s * 16384 + h * 8192, &tmK, kvbar, s * 64, row, it.kvbh);
                     }
                 if (it_cnt >= 1) mbar_wait(smem_u32(&bar_ve), (it_cnt - 1) & 1);
                 for (int h = 0; h < nc; ++h)
                     for (int s = 0; s < C::kSub; ++s) {
                         const int row = (h ? it.c1 : it.c0) * 64;
-                        tma_load_3d(sV + s * 16384 + h * 8192, &tmV, kvbar, s * 64, row, it.kvbh);
+                        if (S2_DKV_L2HINT)
+                            tma_load_3d_hint(sV + s * 16384 + h * 8192, &tmV, kvbar, s * 64, row, it.kvbh, once);
+                        else
+                            tma_load_3d(sV + s * 16384 + h * 8192, &tmV, kvbar, s * 64, row, it.kvbh);
                     }
                 for (int j = 0; j < p.hpg; ++j) {
                     const int qbh = it.kvbh * p.hpg + j;
@@ -291,8 +304,13 @@ __global__ void __launch_bounds__(384, 1)
                             // debug 16 (timing experiments only, wrong results): skip the dO tile
                             const bool half_bytes = (p.debug & 16) != 0;
                             mbar_expect_tx(bar, (half_bytes ? 1 : 2) * C::kTile64 + 512);
-                            tma_load_rows(base, &tmQ, bar, row0, qbh);
-                            if (!half_bytes) tma_load_rows(base + C::kTile64, &tmdO, bar, row0, qbh);
+                            if (S2_DKV_L2HINT) {
+                                tma_load_rows_hint(base, &tmQ, bar, row0, qbh, keep);
+                                if (!half_bytes) tma_load_rows_hint(base + C::kTile64, &tmdO, bar, row0, qbh, keep);
+                            } else {
+                                tma_load_rows(base, &tmQ, bar, row0, qbh);
+                                if (!half_bytes) tma_load_rows(base + C::kTile64, &tmdO, bar, row0, qbh);
+                            }
                             const size_t lo = static_cast<size_t>(qbh) * p.Npad + row0;
                             bulk_load(sAux + st * C::kAux, p.lse2 + lo, 256, bar);
                             bulk_load(sAux + st * C::kAux + 256, p.delta + lo, 256, bar);
