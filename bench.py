@@ -10,9 +10,10 @@ synthetic bf16 inputs.
 
 --workload cfg3 (default): BASELINE.json configs[2] (S=32K, H=32, D=128, block
     64, local_blocks 4, vert_stride 16, heterogeneous head offsets), one layer per
-    GPU.  Under torchrun the (batch, head) units of a global batch of N are
-    LPT-partitioned across ranks by active-block count (weak scaling) and the
-    forward output is all-gathered with NCCL (the north_star's single exchange).
+    GPU.  Under torchrun a global batch of N sequences is sharded one sequence
+    per rank (weak scaling, data parallel): every rank owns complete outputs, so
+    there is no data-path collective (--exchange allgather / fused add the
+    head-parallel output exchange for comparison).
 --workload cfg5: BASELINE.json configs[4] (S=128K, H=32, D=128, B=1), its 32
     heads LPT-split over the ranks by active blocks (strong scaling), all-gather
     of O overlapping the backward.
@@ -231,13 +232,17 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def config_desc(n, exchange="allgather"):
-    how = ("forward stores O into every rank's output (fused exchange)" if exchange == "fused" and n > 1
-           else "all-gather of O")
+def config_desc(n, exchange="none"):
+    if exchange == "none":
+        par = f"data-parallel x{n}: one sequence per GPU, no collective on the data path"
+    else:
+        how = ("forward stores O into every rank's output (fused exchange)" if exchange == "fused" and n > 1
+               else "all-gather of O")
+        par = f"head-parallel x{n} (LPT by active blocks), {how}"
     return {"workload": "cfg3: one S2 attention layer fwd+bwd, S=32768, H=32, D=128, block 64, "
                         "local_blocks 4, vert_stride 16, heterogeneous head offsets",
             "batch_per_gpu": 1, "global_batch": n, "seq_len": N_SEQ, "heads": H, "head_dim": D,
-            "parallelism": f"head-parallel x{n} (LPT by active blocks), {how}",
+            "parallelism": par,
             "l2": "inputs 256 MiB per tensor > 126 MB L2; no flush needed"}
 
 
@@ -388,7 +393,7 @@ def _roofline(kernels, fwd_flops, pk, pk_kind, with_traffic=True):
             "alg_flops_per_launch": alg.get(dom, 0.0)}
 
 
-def _setup_dist():
+def _setup_dist(collective: bool = True):
     import torch
     import torch.distributed as dist
 
@@ -415,7 +420,8 @@ def _setup_dist():
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
-            _abi.check(_abi.lib().s2_set_sm_reserve(int(os.environ["NCCL_MAX_CTAS"])))
+            if collective:  # only a step with an exchange leaves NCCL its SMs
+                _abi.check(_abi.lib().s2_set_sm_reserve(int(os.environ["NCCL_MAX_CTAS"])))
         else:
             dist.init_process_group(backend)
     return world, rank, local, dev
@@ -429,7 +435,7 @@ def run_s2(args):
     from paper_2407_17678_b200 import _abi
     from paper_2407_17678_b200.dist import HeadParallelPlan
 
-    world, rank, local, dev = _setup_dist()
+    world, rank, local, dev = _setup_dist(collective=args.exchange != "none")
     cfg5 = args.workload == "cfg5"
     n_seq = N_CFG5 if cfg5 else N_SEQ
     cfg = s2.make_s2_config(n_seq, H, block_size=BLOCK, local_blocks=LOCAL, vert_stride=VSTRIDE)
@@ -437,7 +443,8 @@ def run_s2(args):
     # cfg3: global batch = world (weak scaling, one layer per GPU);
     # cfg5: one 128K sequence, its 32 heads split over the ranks (strong scaling)
     gbatch = 1 if cfg5 else world
-    hp = HeadParallelPlan(plan, gbatch, world)
+    # cfg3 without an exchange: one whole sequence per rank (data parallel)
+    hp = HeadParallelPlan(plan, gbatch, world, mode="batch" if args.exchange == "none" else "lpt")
     units = hp.units[rank]
     U = len(units)
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -474,7 +481,8 @@ def run_s2(args):
             dist.all_reduce(fence)
             return
         s2.s2_attn_fwd(plan, q, k, v, out=out, lse=lse, unit_ids=units)
-        finish = hp.all_gather_async(out.reshape(U, 1, n_seq, D)) if world > 1 else None
+        exchange = world > 1 and args.exchange != "none"
+        finish = hp.all_gather_async(out.reshape(U, 1, n_seq, D)) if exchange else None
         # the backward needs only this rank's units: it overlaps the all-gather
         s2.s2_attn_bwd(plan, q, k, v, out, lse, do, dq=dq, dk=dk, dv=dv, unit_ids=units)
         if finish is not None:
@@ -536,15 +544,17 @@ def run_s2(args):
     }
     if world > 1 or cfg5:
         # the exchange budget: every rank receives the other ranks' O (bf16) once per step
-        o_bytes = gbatch * H * n_seq * D * 2
-        line["exchange"] = {"all_gather_bytes_total": o_bytes,
+        # (none in the data-parallel cfg3 mode)
+        o_bytes = gbatch * H * n_seq * D * 2 if args.exchange != "none" else 0
+        line["exchange"] = {"mode": args.exchange, "all_gather_bytes_total": o_bytes,
                             "received_bytes_per_gpu": o_bytes * (world - 1) // max(1, world),
-                            "padded_send_bytes_per_gpu": hp.max_units * n_seq * D * 2,
+                            "padded_send_bytes_per_gpu": hp.max_units * n_seq * D * 2 if o_bytes else 0,
                             "overlap_window_ms": bwd_ms,
                             "rank_active_blocks": [int(x) for x in hp.load],
                             "imbalance_max_over_ideal": hp.imbalance(),
                             "nccl_max_ctas": int(os.environ.get("NCCL_MAX_CTAS", "0")) if world > 1 else 0,
-                            "sm_reserve_backward": int(os.environ.get("NCCL_MAX_CTAS", "0")) if world > 1 else 0}
+                            "sm_reserve_backward": (int(os.environ.get("NCCL_MAX_CTAS", "0"))
+                                                    if world > 1 and args.exchange != "none" else 0)}
 
     # ---- end to end through the public API with host buffers
     if not args.no_e2e and not cfg5:
@@ -868,10 +878,14 @@ def main():
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-hybrid", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the cfg1/cfg2/cfg5 lines (N=1)")
-    ap.add_argument("--exchange", default="allgather", choices=["allgather", "fused"],
-                    help="N>1: NCCL all-gather of O overlapped with the backward (default), or the "
-                         "forward storing O straight into every rank's output (s2_attn_fwd_peers)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "none", "allgather", "fused"],
+                    help="N>1: none (cfg3 default: one sequence per rank, nothing to exchange), NCCL "
+                         "all-gather of O overlapped with the backward (cfg5 default: one sequence's "
+                         "heads over the ranks), or the forward storing O straight into every rank's "
+                         "output (s2_attn_fwd_peers)")
     args = ap.parse_args()
+    if args.exchange == "auto":
+        args.exchange = "allgather" if args.workload == "cfg5" else "none"
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -37,13 +37,25 @@ def partition_lpt(weights, num_ranks: int) -> Tuple[np.ndarray, np.ndarray]:
 class HeadParallelPlan:
     """Which (batch, kv-group) units each rank owns, and how to scatter / gather."""
 
-    def __init__(self, plan, batch: int, world_size: int):
+    def __init__(self, plan, batch: int, world_size: int, mode: str = "lpt"):
+        """mode "lpt": units (batch, kv-group) longest-first to the least-loaded rank
+        (one sequence's heads spread over the ranks: the output exchange assembles
+        it).  mode "batch": whole sequences per rank when world_size divides batch
+        (data parallelism: every rank owns complete outputs, nothing to exchange;
+        the loads are equal because every sequence has the same layout)."""
         self.plan = plan
         self.batch = batch
         self.world_size = world_size
         self.hpg = plan.num_heads // plan.num_kv_heads
         self.weights = plan.unit_weights(batch)
-        self.owner, self.load = partition_lpt(self.weights, world_size)
+        if mode == "batch" and batch % world_size == 0:
+            per = batch // world_size * plan.num_kv_heads
+            self.owner = (np.arange(batch * plan.num_kv_heads) // per).astype(np.int32)
+            self.load = np.array([self.weights[self.owner == r].sum() for r in range(world_size)], np.int64)
+        elif mode in ("lpt", "batch"):
+            self.owner, self.load = partition_lpt(self.weights, world_size)
+        else:
+            raise ValueError(f"unknown mode {mode!r}")
         self.units: List[np.ndarray] = [np.nonzero(self.owner == r)[0].astype(np.int32)
                                         for r in range(world_size)]
         self.max_units = max(1, max(len(u) for u in self.units))

@@ -128,3 +128,24 @@ def test_cfg5_shaped_split_32_heads_over_8_ranks_gloo(tmp_path):
     np.testing.assert_array_equal(r["lse"].ravel(), rl.astype(np.float32))
     assert sorted(np.bincount(r["owner"], minlength=8).tolist()) == [4] * 8
     assert r["load"].max() / (r["load"].sum() / 8) < 1.05
+
+
+def test_batch_mode_gives_each_rank_whole_sequences():
+    """HeadParallelPlan(mode="batch"), bench.py's cfg3 default (data parallel): with
+    world_size dividing the batch, rank r owns exactly the (batch, kv-group) units of
+    sequences r*B/W .. (r+1)*B/W - 1, loads are equal (one layout for every sequence),
+    and a batch the ranks do not divide falls back to the LPT split."""
+    import numpy as np
+
+    import paper_2407_17678_b200 as s2
+    from paper_2407_17678_b200.dist import HeadParallelPlan
+
+    plan = s2.Plan.from_config(s2.make_s2_config(4096, 8, local_blocks=2, vert_stride=4, num_kv_heads=4))
+    hp = HeadParallelPlan(plan, 4, 2, mode="batch")
+    assert [u.tolist() for u in hp.units] == [list(range(0, 8)), list(range(8, 16))]
+    assert hp.load[0] == hp.load[1] and hp.imbalance() == 1.0
+    lpt = HeadParallelPlan(plan, 4, 2)
+    odd = HeadParallelPlan(plan, 3, 2, mode="batch")  # 3 sequences over 2 ranks: LPT
+    ref = HeadParallelPlan(plan, 3, 2)
+    assert np.array_equal(odd.owner, ref.owner)
+    assert sorted(np.concatenate(lpt.units).tolist()) == list(range(16))

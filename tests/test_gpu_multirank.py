@@ -93,7 +93,7 @@ def test_head_parallel_world2_on_one_gpu_is_bit_identical(case, tmp_path):
     assert open(res).read() == "ok"
 
 
-@pytest.mark.parametrize("exchange", ["allgather", "fused"])
+@pytest.mark.parametrize("exchange", ["none", "allgather", "fused"])
 def test_bench_world2_prints_one_valid_line(exchange):
     env = dict(os.environ, S2_BENCH_SHARE_GPU="1", S2_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
@@ -108,6 +108,10 @@ def test_bench_world2_prints_one_valid_line(exchange):
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["steps"] == 3
     assert d["config"]["global_batch"] == 2
     assert ("fused" in d["config"]["parallelism"]) == (exchange == "fused")
+    assert d["exchange"]["mode"] == exchange
+    if exchange == "none":  # cfg3's default: one sequence per rank, nothing gathered
+        assert "data-parallel" in d["config"]["parallelism"]
+        assert d["exchange"]["all_gather_bytes_total"] == 0 and d["exchange"]["imbalance_max_over_ideal"] == 1.0
 
 
 def test_bench_cfg5_strong_world2_prints_one_valid_line():
